@@ -1,0 +1,174 @@
+/*
+ * srj.h -- C ABI of the B200 (sm_100a) SRJ weighted-Jacobi sweep library
+ * (libsrj.so).  Plain pointers and sizes only; no torch or Python types.
+ *
+ * The reference (arXiv:1511.04292 package, /root/reference/pkg/src/srj) has no
+ * FFI: its hot path is the numba kernel dispatch in grids.py.  Each entry point
+ * below names the reference interface it replaces (file:line relative to
+ * pkg/src/srj/).  INTEGRATION.md shows the ctypes binding a maintainer adds.
+ *
+ * Conventions
+ *   - Every function returns an int status: SRJ_OK (0) or a negative SRJ_E*
+ *     code; srj_last_error() returns a thread-local message for the last
+ *     failure.  The Python host maps failures to RuntimeError/ValueError with
+ *     the reference's messages.
+ *   - "device" pointers are CUDA global-memory pointers on the current device;
+ *     "host" pointers are CPU memory (pinned for full copy bandwidth).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - Arithmetic is fp64 and bit-identical to the reference kernels _wj2/_wj3
+ *     (grids.py:351-408): r = s - ((((c*u + am0*u[i-1]) + ap0*u[i+1]) +
+ *     am1*u[j-1]) + ap1*u[j+1]) [+ am2*u[k-1] + ap2*u[k+1] in 3D],
+ *     d = (omega*r)/c, un = u + d; no FMA contraction; NaNs never enter the
+ *     max-norms (same as "if abs(d) > dmax").
+ */
+#ifndef SRJ_H
+#define SRJ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRJ_ABI_VERSION 1
+
+enum {
+    SRJ_OK = 0,
+    SRJ_EINVAL = -1,       /* bad argument (maps to ValueError)            */
+    SRJ_ECUDA = -2,        /* CUDA runtime/launch failure                  */
+    SRJ_ENOMEM = -3,       /* device allocation failed                     */
+    SRJ_EUNSUPPORTED = -4  /* feature outside the GPU path (NotImplemented) */
+};
+
+/* ------------------------------------------------------------------------
+ * Device field layout ("padded layout").
+ *
+ * A ghosted field of interior extents n[0..ndim) (axis 0 slowest, as the
+ * reference's C-order arrays) is stored with a 128-byte aligned row pitch so
+ * the first interior cell of every row sits on a 128 B boundary.  Element
+ * (g0, g1[, g2]) in ghost-inclusive reference indices (g = interior index + 1)
+ * lives at   base + origin_shift + g0*plane0 + g1*pitch + g2      (3D)
+ *            base + origin_shift + g0*pitch  + g1                 (2D)
+ * where origin_shift puts g_last = 1 on an aligned address.  Rows along
+ * axis 0 may carry `halo0` >= 1 ghost layers (multi-GPU slabs); the reference
+ * layout corresponds to halo0 = 1.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int32_t ndim;          /* 2 or 3                                          */
+    int32_t halo0;         /* ghost layers on axis 0 (>= 1)                   */
+    int64_t n[3];          /* interior extents                                */
+    int64_t pitch;         /* elements between consecutive last-axis rows      */
+    int64_t plane;         /* elements between axis-0 layers (3D; 2D: = pitch) */
+    int64_t rows0;         /* axis-0 layers allocated = n[0] + 2*halo0         */
+    int64_t origin;        /* element offset of (layer 0, row 0, ghost col 0);
+                              reference index (g0, g1[, g2]) is at layer
+                              g0 + halo0 - 1, so with halo0 == 1 this is the
+                              reference's (0, 0[, 0])                         */
+    int64_t elems;         /* elements to allocate per field                   */
+} srj_layout_t;
+
+/* Computes the padded layout for a grid.  Pure host arithmetic. */
+int srj_layout(int32_t ndim, const int64_t *n, int32_t halo0,
+               srj_layout_t *out);
+
+/* ------------------------------------------------------------------------
+ * Kernel-level entry point: one weighted-Jacobi step on the REFERENCE's dense
+ * layout, replacing one call of the numba dispatch
+ *     _WJ_KERNELS[ndim](u, scratch, *_coefficient_args(problem), omega, reverse)
+ *     (grids.py:478, :547-554; argument order = _coefficient_args,
+ *      grids.py:482-488)
+ * u/un: device, shape n+2 per axis (dense C order).  s, c, lower[ax],
+ * upper[ax]: device, interior-shaped dense.  act: device uint8 interior mask or
+ * NULL.  Writes only the interior of un.  d_norms (device, 2 doubles) receives
+ * (dmax, rmax) of this step.  The reference's `reverse` flag has no effect on
+ * a two-buffer update and is therefore not an argument.
+ * ---------------------------------------------------------------------- */
+int srj_wj_dense(int32_t ndim, const int64_t *n, const double *u, double *un,
+                 const double *s, const double *c, const double *const *lower,
+                 const double *const *upper, const uint8_t *act, double omega,
+                 double *d_norms, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Solver plan: the device side of srj_solve / jacobi_solve / _Sweeper
+ * (grids.py:535-559, :602-694).  Buffers are owned by the caller.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    srj_layout_t layout;         /* from srj_layout()                         */
+    int32_t coef_mode;           /* 0: constant stencil (scalars below)       */
+                                 /* 1: per-cell arrays (coef_arrays)          */
+    double coef[7];              /* center, lower0, upper0, lower1, upper1,
+                                    lower2, upper2 (constant mode)            */
+    const double *coef_arrays[7];/* same order, device, padded layout         */
+    const uint8_t *act;          /* device uint8 mask in padded layout or NULL */
+    const double *source;        /* device, padded layout (interior used)     */
+    const double *kappa;         /* device, padded: nonlinear source
+                                    s = kappa*u^5 from the current iterate
+                                    (source ignored), or NULL                 */
+    int64_t own0_begin;          /* axis-0 interior rows this plan owns for   */
+    int64_t own0_end;            /*   stores and norms (default 0, n[0])      */
+    int32_t physical_lo0;        /* 1: layer below row 0 is a FIXED boundary  */
+    int32_t physical_hi0;        /* 1: layer above row n0-1 is a FIXED bound. */
+} srj_plan_desc;
+
+typedef struct srj_plan srj_plan;
+
+/* Validates the descriptor, allocates small device scratch. */
+int srj_plan_create(const srj_plan_desc *desc, srj_plan **out);
+int srj_plan_destroy(srj_plan *plan);
+
+/* Maximum fused-sweep depth (temporal blocking) supported by srj_plan_run. */
+int srj_max_fuse(void);
+
+/* Runs `nsteps` elementary steps k = first .. first+nsteps-1 with
+ * omega_k = weights[k mod m] (weights: HOST array of the cycle's M weights,
+ * CycleSchedule.weight_sequence, schedule.py:33-83), starting from the field
+ * in `src` and ping-ponging between buf_a and buf_b (both distinct from src,
+ * so src survives as a snapshot).  `fuse` = sweeps fused per launch
+ * (0 = plan default; 1..srj_max_fuse()).  d_norms (device, 2*nsteps doubles)
+ * receives per-step (dmax, rmax) exactly as _wj* returns them; it is
+ * zero-initialised by this call.  *final_buf = 0 (src, nsteps==0), 1 (buf_a)
+ * or 2 (buf_b) tells where the last iterate is.  Asynchronous on `stream`.
+ * Replaces the per-step loop of _iterate/_Sweeper.jacobi
+ * (grids.py:613-617, :544-559). */
+int srj_plan_run(srj_plan *plan, const double *src, double *buf_a,
+                 double *buf_b, const double *weights, int64_t m,
+                 int64_t first, int64_t nsteps, int32_t fuse, double *d_norms,
+                 int32_t *final_buf, void *stream);
+
+/* True residual of field u: d_out[0] = sum r^2, d_out[1] = max |r| over the
+ * owned active cells, r = s - A u (GridProblem.residual_field,
+ * grids.py:249-266; same operator association as the sweep).  Deterministic
+ * two-pass reduction (fixed order).  d_out: device, 2 doubles. */
+int srj_plan_residual(srj_plan *plan, const double *u, double *d_out,
+                      void *stream);
+
+/* Host <-> device transfers between the reference's dense layout and the
+ * padded layout (cudaMemcpy2DAsync; host memory should be pinned).
+ *   field:    ghosted array, shape n+2 per axis (problem.u)
+ *   interior: interior-shaped array (problem.source / center / ...); written
+ *             into the interior positions of a padded field-shaped buffer
+ *   elem_size: 8 for fp64 fields, 1 for the uint8 mask.
+ * For halo0 > 1 layouts only layers [halo0-1, halo0+n0] are transferred. */
+int srj_upload_field(const srj_layout_t *lay, const double *host, double *dev,
+                     void *stream);
+int srj_download_field(const srj_layout_t *lay, const double *dev, double *host,
+                       void *stream);
+int srj_upload_interior(const srj_layout_t *lay, const void *host, void *dev,
+                        int32_t elem_size, void *stream);
+
+/* Copies `count` axis-0 layers starting at layer `first_layer` (padded-layout
+ * layer index, 0 = lowest allocated layer) between two padded buffers of the
+ * same layout, possibly on different devices via peer access (halo exchange
+ * for slab decomposition). */
+int srj_copy_layers(const srj_layout_t *lay, const double *src,
+                    int64_t src_layer, double *dst, int64_t dst_layer,
+                    int64_t count, void *stream);
+
+int srj_abi_version(void);
+const char *srj_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SRJ_H */

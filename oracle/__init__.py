@@ -1,0 +1,20 @@
+"""CPU parity oracle for the SRJ sweep path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
+legs may import this package.  The product package
+(``paper_1511_04292_b200``) never imports it and has no CPU fallback.
+
+Pinned against the reference (``/root/reference/pkg/src/srj``) through the
+golden vectors in ``tests/golden`` that ``tools/make_golden.py`` produced by
+running the reference's own ``srj_solve`` / ``weighted_jacobi_sweep`` here.
+"""
+
+from .oracle import (  # noqa: F401
+    OVERFLOW_LIMIT,
+    load,
+    np_step,
+    residual,
+    run,
+    solve,
+    step,
+)

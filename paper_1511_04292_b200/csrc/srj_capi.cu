@@ -1,0 +1,481 @@
+// srj_capi.cu -- C ABI (include/srj.h) over the sm_100a SRJ kernels.
+//
+// Host-side launch logic for the reference's hot loop (grids.py:535-559,
+// :602-687): the caller (Python, ctypes) owns all device buffers; this layer
+// plans the launch geometry, picks the fused-sweep depth, launches the
+// kernels on the caller's stream and reports errors as status codes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/srj.h"
+#include "srj_reduce.cuh"
+#include "srj_sweep2d.cuh"
+#include "srj_sweep3d.cuh"
+
+using namespace srj;
+
+namespace {
+
+constexpr int64_t kAlign = 16;        // elements (128 B)
+constexpr int64_t kXOff = kAlign - 1; // last-axis ghost g=0 sits at offset 15
+constexpr int64_t kSlack = 256;       // tail elements for band over-reads
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  return fail(e == cudaErrorMemoryAllocation ? SRJ_ENOMEM : SRJ_ECUDA, "%s: %s", what,
+              cudaGetErrorString(e));
+}
+
+#define SRJ_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// offset of interior cell (0,0[,0])
+int64_t interior_offset(const srj_layout_t &l) {
+  return l.origin + int64_t(l.halo0) * l.plane + (l.ndim == 3 ? l.pitch : 0) + 1;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------ 2D dispatch
+using Sweep2DFn = void (*)(const Sweep2DParams &, int blocks, cudaStream_t);
+
+template <int T, bool VAR, bool NL>
+void launch2d(const Sweep2DParams &p, int blocks, cudaStream_t s) {
+  using B = Band2D<T>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(sweep2d_tb<T, VAR, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(B::smem_bytes()));
+    configured = true;
+  }
+  sweep2d_tb<T, VAR, NL><<<blocks, B::WARPS * 32, B::smem_bytes(), s>>>(p);
+}
+
+template <bool VAR, bool NL>
+Sweep2DFn pick2d(int T) {
+  switch (T) {
+    case 1: return launch2d<1, VAR, NL>;
+    case 2: return launch2d<2, VAR, NL>;
+    case 3: return launch2d<3, VAR, NL>;
+    case 4: return launch2d<4, VAR, NL>;
+    case 5: return launch2d<5, VAR, NL>;
+    case 6: return launch2d<6, VAR, NL>;
+    case 7: return launch2d<7, VAR, NL>;
+    case 8: return launch2d<8, VAR, NL>;
+  }
+  return nullptr;
+}
+
+Sweep2DFn pick2d(int T, bool var, bool nl) {
+  if (var) return nl ? pick2d<true, true>(T) : pick2d<true, false>(T);
+  return nl ? pick2d<false, true>(T) : pick2d<false, false>(T);
+}
+
+template <int T>
+int own_cols() { return Band2D<T>::OWN; }
+
+int band_own(int T) {
+  switch (T) {
+    case 1: return own_cols<1>();
+    case 2: return own_cols<2>();
+    case 3: return own_cols<3>();
+    case 4: return own_cols<4>();
+    case 5: return own_cols<5>();
+    case 6: return own_cols<6>();
+    case 7: return own_cols<7>();
+    default: return own_cols<8>();
+  }
+}
+
+int blocks_per_sm_2d(int T) {
+  // shared-memory bound occupancy of the band kernel (4 warps per block)
+  size_t bytes = 0;
+  switch (T) {
+    case 1: bytes = Band2D<1>::smem_bytes(); break;
+    case 2: bytes = Band2D<2>::smem_bytes(); break;
+    case 3: bytes = Band2D<3>::smem_bytes(); break;
+    case 4: bytes = Band2D<4>::smem_bytes(); break;
+    case 5: bytes = Band2D<5>::smem_bytes(); break;
+    case 6: bytes = Band2D<6>::smem_bytes(); break;
+    case 7: bytes = Band2D<7>::smem_bytes(); break;
+    default: bytes = Band2D<8>::smem_bytes(); break;
+  }
+  int b = int((227 * 1024) / (bytes + 1024));
+  return std::max(1, std::min(b, 8));
+}
+
+}  // namespace
+
+struct srj_plan {
+  srj_plan_desc d;
+  int default_fuse;
+  double *partials;  // [kResidBlocks][2] device scratch
+};
+
+extern "C" {
+
+int srj_abi_version(void) { return SRJ_ABI_VERSION; }
+const char *srj_last_error(void) { return g_err; }
+int srj_max_fuse(void) { return kMaxFuse; }
+
+int srj_layout(int32_t ndim, const int64_t *n, int32_t halo0, srj_layout_t *out) {
+  if (!out || !n) return fail(SRJ_EINVAL, "null argument");
+  if (ndim != 2 && ndim != 3)
+    return fail(SRJ_EUNSUPPORTED, "the GPU path supports 2- and 3-dimensional grids (got %d)", ndim);
+  if (halo0 < 1 || halo0 > kMaxFuse) return fail(SRJ_EINVAL, "halo0 must be in [1, %d]", kMaxFuse);
+  srj_layout_t l;
+  std::memset(&l, 0, sizeof(l));
+  l.ndim = ndim;
+  l.halo0 = halo0;
+  for (int a = 0; a < ndim; ++a) {
+    if (n[a] < 1 || n[a] > (int64_t(1) << 30)) return fail(SRJ_EINVAL, "bad extent n[%d]=%lld", a, (long long)n[a]);
+    l.n[a] = n[a];
+  }
+  const int64_t last = n[ndim - 1];
+  l.pitch = kAlign + round_up(last + 1, 64);
+  l.plane = (ndim == 3) ? (n[1] + 2) * l.pitch : l.pitch;
+  l.rows0 = n[0] + 2 * int64_t(halo0);
+  l.origin = kXOff;
+  l.elems = l.rows0 * l.plane + kSlack + kAlign;
+  *out = l;
+  return SRJ_OK;
+}
+
+int srj_wj_dense(int32_t ndim, const int64_t *n, const double *u, double *un, const double *s,
+                 const double *c, const double *const *lower, const double *const *upper,
+                 const uint8_t *act, double omega, double *d_norms, void *stream) {
+  if (ndim != 2 && ndim != 3)
+    return fail(SRJ_EUNSUPPORTED, "the GPU path supports 2- and 3-dimensional grids (got %d)", ndim);
+  if (!u || !un || !s || !c || !lower || !upper || !d_norms) return fail(SRJ_EINVAL, "null argument");
+  DenseParams p{};
+  p.u = u;
+  p.un = un;
+  p.s = s;
+  p.c = c;
+  for (int a = 0; a < ndim; ++a) {
+    p.lo[a] = lower[a];
+    p.hi[a] = upper[a];
+  }
+  p.act = act;
+  p.ndim = ndim;
+  p.n0 = n[0];
+  p.n1 = n[1];
+  p.n2 = (ndim == 3) ? n[2] : 1;
+  p.omega = omega;
+  p.norms = d_norms;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SRJ_CUDA(cudaMemsetAsync(d_norms, 0, 2 * sizeof(double), st));
+  const int64_t total = p.n0 * p.n1 * p.n2;
+  if (total == 0) return SRJ_OK;
+  const int blocks = int(std::min<int64_t>((total + 255) / 256, int64_t(sm_count()) * 16));
+  wj_dense<<<blocks, 256, 0, st>>>(p);
+  SRJ_CUDA(cudaGetLastError());
+  return SRJ_OK;
+}
+
+int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
+  if (!desc || !out) return fail(SRJ_EINVAL, "null argument");
+  const srj_layout_t &l = desc->layout;
+  if (l.ndim != 2 && l.ndim != 3) return fail(SRJ_EUNSUPPORTED, "ndim must be 2 or 3");
+  if (!desc->source && !desc->kappa) return fail(SRJ_EINVAL, "source (or kappa) required");
+  if (desc->coef_mode != 0 && desc->coef_mode != 1) return fail(SRJ_EINVAL, "coef_mode must be 0 or 1");
+  if (desc->coef_mode == 1)
+    for (int a = 0; a < 1 + 2 * l.ndim; ++a)
+      if (!desc->coef_arrays[a]) return fail(SRJ_EINVAL, "coefficient array %d missing", a);
+  if (desc->coef_mode == 0 && desc->coef[0] == 0.0)
+    return fail(SRJ_EINVAL, "center coefficient vanishes on an active cell");
+  srj_plan *p = new (std::nothrow) srj_plan;
+  if (!p) return fail(SRJ_ENOMEM, "host allocation failed");
+  p->d = *desc;
+  if (p->d.own0_end <= p->d.own0_begin) {
+    p->d.own0_begin = 0;
+    p->d.own0_end = l.n[0];
+  }
+  if (p->d.own0_begin < 0 || p->d.own0_end > l.n[0]) {
+    delete p;
+    return fail(SRJ_EINVAL, "owned rows out of range");
+  }
+  p->default_fuse = (l.ndim == 2 && desc->coef_mode == 0) ? 4 : 1;
+  p->partials = nullptr;
+  cudaError_t e = cudaMalloc(&p->partials, sizeof(double) * 2 * kResidBlocks);
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "cudaMalloc(partials)");
+  }
+  *out = p;
+  return SRJ_OK;
+}
+
+int srj_plan_destroy(srj_plan *p) {
+  if (!p) return SRJ_OK;
+  if (p->partials) cudaFree(p->partials);
+  delete p;
+  return SRJ_OK;
+}
+
+static void row_ranges(const srj_plan_desc &d, int &lo_c, int &hi_c, int &ld_lo, int &ld_hi) {
+  const srj_layout_t &l = d.layout;
+  const int n0 = int(l.n[0]), h = l.halo0;
+  if (d.physical_lo0) {
+    lo_c = 0;
+    ld_lo = -1;
+  } else {
+    lo_c = -h;
+    ld_lo = -h;
+  }
+  if (d.physical_hi0) {
+    hi_c = n0;
+    ld_hi = n0;
+  } else {
+    hi_c = n0 + h;
+    ld_hi = n0 + h - 1;
+  }
+}
+
+int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b,
+                 const double *weights, int64_t m, int64_t first, int64_t nsteps, int32_t fuse,
+                 double *d_norms, int32_t *final_buf, void *stream) {
+  if (!plan || !src || !buf_a || !buf_b || !weights || !final_buf)
+    return fail(SRJ_EINVAL, "null argument");
+  if (m < 1) return fail(SRJ_EINVAL, "weight cycle must be non-empty");
+  if (nsteps < 0 || first < 0) return fail(SRJ_EINVAL, "negative step range");
+  if (src == buf_a || src == buf_b || buf_a == buf_b)
+    return fail(SRJ_EINVAL, "src, buf_a and buf_b must be distinct");
+  *final_buf = 0;
+  if (nsteps == 0) return SRJ_OK;
+  if (!d_norms) return fail(SRJ_EINVAL, "null norms buffer");
+  const srj_plan_desc &d = plan->d;
+  const srj_layout_t &l = d.layout;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int T = fuse > 0 ? fuse : plan->default_fuse;
+  if (l.ndim == 3) T = 1;
+  if (T > kMaxFuse) return fail(SRJ_EINVAL, "fuse depth %d exceeds %d", T, kMaxFuse);
+  if ((!d.physical_lo0 || !d.physical_hi0) && T > l.halo0)
+    return fail(SRJ_EINVAL, "fuse depth %d needs halo0 >= %d on exchanged faces", T, T);
+
+  SRJ_CUDA(cudaMemsetAsync(d_norms, 0, sizeof(double) * 2 * size_t(nsteps), st));
+  const int64_t ioff = interior_offset(l);
+  const bool var = d.coef_mode == 1;
+  const bool nl = d.kappa != nullptr;
+  const double *f = nl ? d.kappa : d.source;
+  int lo_c, hi_c, ld_lo, ld_hi;
+  row_ranges(d, lo_c, hi_c, ld_lo, ld_hi);
+  const int rows = int(d.own0_end - d.own0_begin);
+
+  const double *cur = src;
+  double *nxt = buf_a;
+  int which = 1;
+  int64_t k = 0;
+  while (k < nsteps) {
+    const int t = int(std::min<int64_t>(T, nsteps - k));
+    if (l.ndim == 2) {
+      Sweep2DParams p{};
+      p.src = cur + ioff;
+      p.dst = nxt + ioff;
+      p.f = f + ioff;
+      p.act = d.act ? d.act + ioff : nullptr;
+      if (var) {
+        p.c = d.coef_arrays[0] + ioff;
+        p.am0 = d.coef_arrays[1] + ioff;
+        p.ap0 = d.coef_arrays[2] + ioff;
+        p.am1 = d.coef_arrays[3] + ioff;
+        p.ap1 = d.coef_arrays[4] + ioff;
+      }
+      p.kc = d.coef[0];
+      p.kam0 = d.coef[1];
+      p.kap0 = d.coef[2];
+      p.kam1 = d.coef[3];
+      p.kap1 = d.coef[4];
+      p.pitch = l.pitch;
+      p.n0 = int(l.n[0]);
+      p.n1 = int(l.n[1]);
+      p.lo_c = lo_c;
+      p.hi_c = hi_c;
+      p.ld_lo = ld_lo;
+      p.ld_hi = ld_hi;
+      p.own_b = int(d.own0_begin);
+      p.own_e = int(d.own0_end);
+      const int own = band_own(t);
+      p.nbands = int((l.n[1] + own - 1) / own);
+      const int target = sm_count() * blocks_per_sm_2d(t) * Band2D<1>::WARPS;
+      int nstrips = std::max(1, (target + p.nbands / 2) / p.nbands);
+      nstrips = std::min(nstrips, std::max(1, rows / std::max(2 * t, 8)));
+      p.H = (rows + nstrips - 1) / nstrips;
+      p.nstrips = (rows + p.H - 1) / p.H;
+      for (int q = 0; q < t; ++q) p.omega[q] = weights[(first + k + q) % m];
+      p.norms = d_norms + 2 * k;
+      const int warps = p.nbands * p.nstrips;
+      const int blocks = (warps + Band2D<1>::WARPS - 1) / Band2D<1>::WARPS;
+      pick2d(t, var, nl)(p, blocks, st);
+    } else {
+      Sweep3DParams p{};
+      p.src = cur + ioff;
+      p.dst = nxt + ioff;
+      p.f = f + ioff;
+      p.act = d.act ? d.act + ioff : nullptr;
+      for (int a = 0; a < 7; ++a) {
+        p.coef[a] = var ? d.coef_arrays[a] + ioff : nullptr;
+        p.kc[a] = d.coef[a];
+      }
+      p.pitch = l.pitch;
+      p.plane = l.plane;
+      p.n0 = int(l.n[0]);
+      p.n1 = int(l.n[1]);
+      p.n2 = int(l.n[2]);
+      // one-deep stencil: only owned rows relax; exchanged halos are inputs
+      p.lo_c = 0;
+      p.hi_c = p.n0;
+      p.ld_lo = ld_lo;
+      p.ld_hi = ld_hi;
+      p.own_b = int(d.own0_begin);
+      p.own_e = int(d.own0_end);
+      p.nbands = int((l.n[2] + 63) / 64);
+      const long per_strip = long(p.n1) * p.nbands;
+      const long target = long(sm_count()) * 48;
+      int nstrips = int(std::max<long>(1, (target + per_strip / 2) / per_strip));
+      nstrips = std::min(nstrips, rows);
+      p.H = (rows + nstrips - 1) / nstrips;
+      p.nstrips = (rows + p.H - 1) / p.H;
+      p.omega = weights[(first + k) % m];
+      p.norms = d_norms + 2 * k;
+      const long warps = per_strip * p.nstrips;
+      const long blocks = (warps + kWarps3D - 1) / kWarps3D;
+      if (var)
+        nl ? sweep3d<true, true><<<blocks, kWarps3D * 32, 0, st>>>(p)
+           : sweep3d<true, false><<<blocks, kWarps3D * 32, 0, st>>>(p);
+      else
+        nl ? sweep3d<false, true><<<blocks, kWarps3D * 32, 0, st>>>(p)
+           : sweep3d<false, false><<<blocks, kWarps3D * 32, 0, st>>>(p);
+    }
+    SRJ_CUDA(cudaGetLastError());
+    k += t;
+    *final_buf = which;
+    cur = nxt;
+    nxt = (which == 1) ? buf_b : buf_a;
+    which = (which == 1) ? 2 : 1;
+  }
+  return SRJ_OK;
+}
+
+int srj_plan_residual(srj_plan *plan, const double *u, double *d_out, void *stream) {
+  if (!plan || !u || !d_out) return fail(SRJ_EINVAL, "null argument");
+  const srj_plan_desc &d = plan->d;
+  const srj_layout_t &l = d.layout;
+  const int64_t ioff = interior_offset(l);
+  ResidParams p{};
+  p.u = u + ioff;
+  const bool nl = d.kappa != nullptr;
+  p.f = (nl ? d.kappa : d.source) + ioff;
+  p.act = d.act ? d.act + ioff : nullptr;
+  const bool var = d.coef_mode == 1;
+  for (int a = 0; a < 7; ++a) {
+    p.coef[a] = (var && a < 1 + 2 * l.ndim) ? d.coef_arrays[a] + ioff : nullptr;
+    p.kc[a] = d.coef[a];
+  }
+  p.pitch = l.pitch;
+  p.plane = l.plane;
+  p.ndim = l.ndim;
+  p.n0 = int(l.n[0]);
+  p.n1 = int(l.n[1]);
+  p.n2 = (l.ndim == 3) ? int(l.n[2]) : 1;
+  p.own_b = int(d.own0_begin);
+  p.own_e = int(d.own0_end);
+  p.partials = plan->partials;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (var)
+    nl ? residual_partial<true, true><<<kResidBlocks, kResidThreads, 0, st>>>(p)
+       : residual_partial<true, false><<<kResidBlocks, kResidThreads, 0, st>>>(p);
+  else
+    nl ? residual_partial<false, true><<<kResidBlocks, kResidThreads, 0, st>>>(p)
+       : residual_partial<false, false><<<kResidBlocks, kResidThreads, 0, st>>>(p);
+  residual_final<<<1, 32, 0, st>>>(plan->partials, kResidBlocks, d_out);
+  SRJ_CUDA(cudaGetLastError());
+  return SRJ_OK;
+}
+
+int srj_upload_field(const srj_layout_t *lay, const double *host, double *dev, void *stream) {
+  if (!lay || !host || !dev) return fail(SRJ_EINVAL, "null argument");
+  const srj_layout_t &l = *lay;
+  const int64_t last = l.n[l.ndim - 1] + 2;
+  const int64_t rows = (l.ndim == 3) ? (l.n[0] + 2) * (l.n[1] + 2) : (l.n[0] + 2);
+  double *dst = dev + l.origin + int64_t(l.halo0 - 1) * l.plane;
+  SRJ_CUDA(cudaMemcpy2DAsync(dst, l.pitch * 8, host, last * 8, last * 8, rows,
+                             cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
+  return SRJ_OK;
+}
+
+int srj_download_field(const srj_layout_t *lay, const double *dev, double *host, void *stream) {
+  if (!lay || !host || !dev) return fail(SRJ_EINVAL, "null argument");
+  const srj_layout_t &l = *lay;
+  const int64_t last = l.n[l.ndim - 1] + 2;
+  const int64_t rows = (l.ndim == 3) ? (l.n[0] + 2) * (l.n[1] + 2) : (l.n[0] + 2);
+  const double *src = dev + l.origin + int64_t(l.halo0 - 1) * l.plane;
+  SRJ_CUDA(cudaMemcpy2DAsync(host, last * 8, src, l.pitch * 8, last * 8, rows,
+                             cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+  return SRJ_OK;
+}
+
+int srj_upload_interior(const srj_layout_t *lay, const void *host, void *dev, int32_t elem_size,
+                        void *stream) {
+  if (!lay || !host || !dev) return fail(SRJ_EINVAL, "null argument");
+  if (elem_size != 1 && elem_size != 8) return fail(SRJ_EINVAL, "elem_size must be 1 or 8");
+  const srj_layout_t &l = *lay;
+  const int64_t e = elem_size;
+  const int64_t ioff = interior_offset(l);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const char *h = static_cast<const char *>(host);
+  char *dv = static_cast<char *>(dev);
+  if (l.ndim == 2) {
+    SRJ_CUDA(cudaMemcpy2DAsync(dv + ioff * e, l.pitch * e, h, l.n[1] * e, l.n[1] * e, l.n[0],
+                               cudaMemcpyHostToDevice, st));
+  } else {
+    const int64_t layer = l.n[1] * l.n[2] * e;
+    for (int64_t i = 0; i < l.n[0]; ++i)
+      SRJ_CUDA(cudaMemcpy2DAsync(dv + (ioff + i * l.plane) * e, l.pitch * e, h + i * layer,
+                                 l.n[2] * e, l.n[2] * e, l.n[1], cudaMemcpyHostToDevice, st));
+  }
+  return SRJ_OK;
+}
+
+int srj_copy_layers(const srj_layout_t *lay, const double *src, int64_t src_layer, double *dst,
+                    int64_t dst_layer, int64_t count, void *stream) {
+  if (!lay || !src || !dst) return fail(SRJ_EINVAL, "null argument");
+  const srj_layout_t &l = *lay;
+  if (count < 0 || src_layer < 0 || dst_layer < 0 || src_layer + count > l.rows0 ||
+      dst_layer + count > l.rows0)
+    return fail(SRJ_EINVAL, "layer range out of bounds");
+  if (count == 0) return SRJ_OK;
+  SRJ_CUDA(cudaMemcpyAsync(dst + l.origin + dst_layer * l.plane, src + l.origin + src_layer * l.plane,
+                           sizeof(double) * size_t(count * l.plane), cudaMemcpyDefault,
+                           static_cast<cudaStream_t>(stream)));
+  return SRJ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,173 @@
+// srj_reduce.cuh -- true-residual norms and the dense-layout single step.
+//
+// residual_partial / residual_final: (sum r^2, max |r|) of r = s - A u over
+// the owned active cells (GridProblem.residual_field, grids.py:249-266, same
+// association as the sweep).  Warp-shuffle -> block -> grid reduction in a
+// FIXED order (thread-strided partial sums, shuffle tree, shared-memory tree,
+// then one block summing the per-block partials in index order), so the L2
+// norm is bit-reproducible run to run.
+//
+// wj_dense: one weighted-Jacobi step on the reference's dense layout, the
+// drop-in for one call of _WJ_KERNELS[ndim] (grids.py:478, :547-554).
+#pragma once
+#include "srj_device.cuh"
+
+namespace srj {
+
+struct ResidParams {
+  const double *u;       // interior origin
+  const double *f;       // source or kappa
+  const uint8_t *act;
+  const double *coef[7];
+  double kc[7];
+  int64_t pitch, plane;  // 2D: plane == pitch
+  int ndim, n0, n1, n2;  // 2D: n2 == 1 and the grid is (n0, n1)
+  int own_b, own_e;
+  double *partials;      // [gridDim.x][2]
+};
+
+constexpr int kResidThreads = 256;
+constexpr int kResidBlocks = 592;  // 4 x 148 SMs; fixed => fixed reduction order
+
+template <bool VAR, bool NL>
+__global__ void __launch_bounds__(kResidThreads) residual_partial(const __grid_constant__ ResidParams p) {
+  double ss = 0.0, mx = 0.0;
+  const int ncols = (p.ndim == 2) ? p.n1 : p.n2;
+  const long nrows = (p.ndim == 2) ? long(p.own_e - p.own_b) : long(p.own_e - p.own_b) * p.n1;
+  for (long row = blockIdx.x; row < nrows; row += gridDim.x) {
+    int i, j;
+    int64_t base;
+    if (p.ndim == 2) {
+      i = p.own_b + int(row);
+      j = 0;
+      base = int64_t(i) * p.pitch;
+    } else {
+      i = p.own_b + int(row / p.n1);
+      j = int(row % p.n1);
+      base = int64_t(i) * p.plane + int64_t(j) * p.pitch;
+    }
+    for (int k = threadIdx.x; k < ncols; k += blockDim.x) {
+      const int64_t q = base + k;
+      if (p.act && !p.act[q]) continue;
+      double kk[7];
+      if constexpr (VAR) {
+        for (int a = 0; a < 7; ++a) kk[a] = (a < 1 + 2 * p.ndim) ? p.coef[a][q] : 0.0;
+      } else {
+        for (int a = 0; a < 7; ++a) kk[a] = p.kc[a];
+      }
+      const double *c = p.u + q;
+      const double uc = c[0];
+      const double s = NL ? nl_source(p.f[q], uc) : p.f[q];
+      double r;
+      if (p.ndim == 2)
+        r = resid5(s, kk[0], uc, kk[1], c[-p.pitch], kk[2], c[p.pitch], kk[3], c[-1], kk[4], c[1]);
+      else
+        r = resid7(s, kk[0], uc, kk[1], c[-p.plane], kk[2], c[p.plane], kk[3], c[-p.pitch],
+                   kk[4], c[p.pitch], kk[5], c[-1], kk[6], c[1]);
+      ss = __dadd_rn(ss, __dmul_rn(r, r));
+      acc_max(mx, r);
+    }
+  }
+  // block reduction, fixed tree
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss = __dadd_rn(ss, __shfl_down_sync(kFull, ss, o));
+    const double w = __shfl_down_sync(kFull, mx, o);
+    mx = (w > mx) ? w : mx;
+  }
+  __shared__ double s_ss[kResidThreads / 32], s_mx[kResidThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_ss[warp] = ss;
+    s_mx[warp] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, m = 0.0;
+    for (int w = 0; w < kResidThreads / 32; ++w) {
+      a = __dadd_rn(a, s_ss[w]);
+      m = (s_mx[w] > m) ? s_mx[w] : m;
+    }
+    p.partials[2 * blockIdx.x] = a;
+    p.partials[2 * blockIdx.x + 1] = m;
+  }
+}
+
+__global__ void __launch_bounds__(32) residual_final(const double *partials, int n, double *out) {
+  // one warp, fixed order: lane l sums partials l, l+32, ... then a shuffle tree
+  double ss = 0.0, mx = 0.0;
+  for (int b = threadIdx.x; b < n; b += 32) {
+    ss = __dadd_rn(ss, partials[2 * b]);
+    const double m = partials[2 * b + 1];
+    mx = (m > mx) ? m : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss = __dadd_rn(ss, __shfl_down_sync(kFull, ss, o));
+    const double w = __shfl_down_sync(kFull, mx, o);
+    mx = (w > mx) ? w : mx;
+  }
+  if (threadIdx.x == 0) {
+    out[0] = ss;
+    out[1] = mx;
+  }
+}
+
+struct DenseParams {
+  const double *u;
+  double *un;
+  const double *s, *c;
+  const double *lo[3], *hi[3];
+  const uint8_t *act;
+  int ndim;
+  int64_t n0, n1, n2;  // 2D: n2 == 1
+  double omega;
+  double *norms;
+};
+
+__global__ void __launch_bounds__(256) wj_dense(const __grid_constant__ DenseParams p) {
+  const int64_t total = p.n0 * p.n1 * p.n2;
+  double dmx = 0.0, rmx = 0.0;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    int64_t g;  // offset of the cell in the ghosted array
+    int64_t s0, s1;  // ghosted strides of axis 0 / axis 1
+    if (p.ndim == 2) {
+      const int64_t i = q / p.n1, j = q % p.n1;
+      s1 = 1;
+      s0 = p.n1 + 2;
+      g = (i + 1) * s0 + (j + 1);
+    } else {
+      const int64_t k = q % p.n2, ij = q / p.n2;
+      const int64_t j = ij % p.n1, i = ij / p.n1;
+      s1 = p.n2 + 2;
+      s0 = (p.n1 + 2) * s1;
+      g = (i + 1) * s0 + (j + 1) * s1 + (k + 1);
+    }
+    const double uc = p.u[g];
+    if (p.act && !p.act[q]) {
+      p.un[g] = uc;
+      continue;
+    }
+    double r;
+    if (p.ndim == 2)
+      r = resid5(p.s[q], p.c[q], uc, p.lo[0][q], p.u[g - s0], p.hi[0][q], p.u[g + s0],
+                 p.lo[1][q], p.u[g - 1], p.hi[1][q], p.u[g + 1]);
+    else
+      r = resid7(p.s[q], p.c[q], uc, p.lo[0][q], p.u[g - s0], p.hi[0][q], p.u[g + s0],
+                 p.lo[1][q], p.u[g - s1], p.hi[1][q], p.u[g + s1], p.lo[2][q], p.u[g - 1],
+                 p.hi[2][q], p.u[g + 1]);
+    const double d = relax(p.omega, r, p.c[q]);
+    p.un[g] = __dadd_rn(uc, d);
+    acc_max(dmx, d);
+    acc_max(rmx, r);
+  }
+  dmx = warp_max(dmx);
+  rmx = warp_max(rmx);
+  if ((threadIdx.x & 31) == 0) {
+    global_max(p.norms, dmx);
+    global_max(p.norms + 1, rmx);
+  }
+}
+
+}  // namespace srj

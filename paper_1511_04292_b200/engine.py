@@ -1,0 +1,206 @@
+"""Device-resident grid state and launch plan (torch owns memory, libsrj computes).
+
+``DeviceGrid`` is the device half of the reference's ``_Sweeper``
+(``grids.py:535-559``): it holds the field in HBM in the padded layout of
+``include/srj.h`` -- three field buffers instead of the reference's two, so the
+iterate at the start of a chunk survives as a snapshot and a solve can stop at
+the exact step the stopping rule fires (see ``grids.srj_solve``) -- plus the
+source / nonlinear factor, the stencil (scalars when constant, per-cell arrays
+otherwise) and the mask.
+
+torch is used only as the device allocator and stream provider.  There is no
+CPU path: constructing a DeviceGrid without a CUDA device raises.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["DeviceGrid", "constant_value", "require_cuda"]
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("the SRJ GPU path needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def constant_value(a):
+    """The scalar if every element of ``a`` has the same fp64 bit pattern."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.size == 0:
+        return None
+    first = a.reshape(-1)[:1]
+    if all(s == 0 for s in a.strides):
+        return float(first[0])
+    bits = a.view(np.int64) if a.flags.c_contiguous else np.ascontiguousarray(a).view(np.int64)
+    if bool(np.all(bits == first.view(np.int64)[0])):
+        return float(first[0])
+    return None
+
+
+def _contig(a, dtype):
+    return np.ascontiguousarray(np.asarray(a, dtype=dtype))
+
+
+class DeviceGrid:
+    """Field, coefficients and launch plan of one grid on one GPU.
+
+    Parameters
+    ----------
+    u : ndarray
+        Ghosted field (interior shape + 2 per axis), FIXED ghosts included.
+    source, center, lower, upper, active :
+        As the reference GridProblem (``grids.py:155-165``); ``active`` is the
+        interior bool mask or None.
+    kappa : ndarray, optional
+        Nonlinear factor: the source becomes kappa * u^5 of the current
+        iterate (``source`` is then ignored).
+    halo0, own, physical : slab-decomposition knobs (``distributed.py``).
+    """
+
+    def __init__(self, u, source, center, lower, upper, active=None, kappa=None,
+                 halo0=1, own=None, physical=(True, True), device=None):
+        torch = require_cuda()
+        lib = _lib.load()
+        self.torch = torch
+        self.lib = lib
+        nd = np.ndim(center)
+        if nd not in (2, 3):
+            raise NotImplementedError(
+                "the GPU path supports 2- and 3-dimensional grids")
+        self.shape = tuple(int(s) for s in np.shape(center))
+        self.ndim = nd
+        self.device = torch.device("cuda", torch.cuda.current_device()
+                                   if device is None else device)
+        n = (ctypes.c_int64 * 3)(*(list(self.shape) + [0] * (3 - nd)))
+        self.layout = _lib.SrjLayout()
+        _lib.check(lib.srj_layout(nd, n, int(halo0), ctypes.byref(self.layout)),
+                   "srj_layout")
+        elems = int(self.layout.elems)
+        with torch.cuda.device(self.device):
+            self.stream = torch.cuda.current_stream(self.device)
+            self._keep = []
+            self.fields = [torch.zeros(elems, dtype=torch.float64, device=self.device)
+                           for _ in range(3)]
+            host_u = _contig(u, np.float64)
+            for f in self.fields:
+                self.upload_field(host_u, f)
+
+            desc = _lib.SrjPlanDesc()
+            desc.layout = self.layout
+            coefs = [center] + [x for ax in range(nd) for x in (lower[ax], upper[ax])]
+            consts = [constant_value(c) for c in coefs]
+            masked = active is not None and not bool(np.all(active))
+            self.constant = all(c is not None for c in consts) and not masked
+            if self.constant:
+                desc.coef_mode = 0
+                for i, c in enumerate(consts):
+                    desc.coef[i] = c
+            else:
+                desc.coef_mode = 1
+                for i, c in enumerate(coefs):
+                    t = self._interior_array(c)
+                    desc.coef_arrays[i] = t.data_ptr()
+            if masked:
+                m = torch.zeros(elems, dtype=torch.uint8, device=self.device)
+                self._upload_interior(_contig(active, np.uint8), m, 1)
+                self._keep.append(m)
+                desc.act = m.data_ptr()
+            if kappa is not None:
+                desc.kappa = self._interior_array(kappa).data_ptr()
+            else:
+                desc.source = self._interior_array(source).data_ptr()
+            lo, hi = (0, self.shape[0]) if own is None else own
+            desc.own0_begin = int(lo)
+            desc.own0_end = int(hi)
+            desc.physical_lo0 = int(bool(physical[0]))
+            desc.physical_hi0 = int(bool(physical[1]))
+            self.desc = desc
+            plan = ctypes.c_void_p()
+            _lib.check(lib.srj_plan_create(ctypes.byref(desc), ctypes.byref(plan)),
+                       "srj_plan_create")
+            self.plan = plan
+            self.norms = torch.zeros(2, dtype=torch.float64, device=self.device)
+            self.resid_out = torch.zeros(2, dtype=torch.float64, device=self.device)
+
+    # ------------------------------------------------------------- transfers
+    @property
+    def _sp(self):
+        return ctypes.c_void_p(self.stream.cuda_stream)
+
+    def _interior_array(self, a):
+        t = self.torch.zeros(int(self.layout.elems), dtype=self.torch.float64,
+                             device=self.device)
+        self._upload_interior(_contig(a, np.float64), t, 8)
+        self._keep.append(t)
+        return t
+
+    def _upload_interior(self, host, dev, esize):
+        _lib.check(self.lib.srj_upload_interior(
+            ctypes.byref(self.layout), host.ctypes.data_as(ctypes.c_void_p),
+            ctypes.c_void_p(dev.data_ptr()), esize, self._sp), "srj_upload_interior")
+        self.stream.synchronize()  # host array may be a temporary
+
+    def upload_field(self, host, dev):
+        _lib.check(self.lib.srj_upload_field(
+            ctypes.byref(self.layout), host.ctypes.data_as(ctypes.c_void_p),
+            ctypes.c_void_p(dev.data_ptr()), self._sp), "srj_upload_field")
+        self.stream.synchronize()
+
+    def download_field(self, idx, host):
+        """Copy field buffer ``idx`` into the ghosted host array (in place)."""
+        if not (host.flags.c_contiguous and host.dtype == np.float64):
+            tmp = np.empty(host.shape, dtype=np.float64)
+            self.download_field(idx, tmp)
+            host[...] = tmp
+            return
+        _lib.check(self.lib.srj_download_field(
+            ctypes.byref(self.layout), ctypes.c_void_p(self.fields[idx].data_ptr()),
+            host.ctypes.data_as(ctypes.c_void_p), self._sp), "srj_download_field")
+        self.stream.synchronize()
+
+    # -------------------------------------------------------------- compute
+    def ensure_norms(self, nsteps):
+        if self.norms.numel() < 2 * nsteps:
+            self.norms = self.torch.zeros(2 * nsteps, dtype=self.torch.float64,
+                                          device=self.device)
+
+    def run(self, src, weights, first, nsteps, fuse=0):
+        """Run steps [first, first+nsteps) from buffer ``src``; returns the
+        buffer index holding the result.  Norms land in ``self.norms``."""
+        self.ensure_norms(max(nsteps, 1))
+        a, b = [i for i in range(3) if i != src]
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        out = ctypes.c_int32(0)
+        f = self.fields
+        _lib.check(self.lib.srj_plan_run(
+            self.plan, ctypes.c_void_p(f[src].data_ptr()),
+            ctypes.c_void_p(f[a].data_ptr()), ctypes.c_void_p(f[b].data_ptr()),
+            w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(w), int(first),
+            int(nsteps), int(fuse), ctypes.c_void_p(self.norms.data_ptr()),
+            ctypes.byref(out), self._sp), "srj_plan_run")
+        return (src, a, b)[out.value]
+
+    def residual(self, idx):
+        """(sum r^2, max|r|) of field buffer ``idx`` (synchronous)."""
+        _lib.check(self.lib.srj_plan_residual(
+            self.plan, ctypes.c_void_p(self.fields[idx].data_ptr()),
+            ctypes.c_void_p(self.resid_out.data_ptr()), self._sp), "srj_plan_residual")
+        v = self.resid_out.cpu().numpy()
+        return float(v[0]), float(v[1])
+
+    def close(self):
+        if getattr(self, "plan", None) is not None:
+            self.lib.srj_plan_destroy(self.plan)
+            self.plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

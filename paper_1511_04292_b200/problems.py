@@ -1,0 +1,129 @@
+"""Seeded synthetic inputs for the BASELINE configurations.
+
+Conventions (recorded in DESIGN.md, "Inputs"):
+
+* unit square / cube, vertex-centred interior nodes x_i = i*h, i = 1..N,
+  h = 1/(N+1) per axis; the ghost layer is the boundary node (FIXED ghosts),
+  as ``srj/problems.py:279-330`` (poisson2d_dirichlet) does;
+* operator in the reference's sign convention (``grids.py:249-262``):
+  center = sum_ax 2/h_ax^2, lower = upper = -1/h_ax^2, source = -f for
+  Laplace(u) = f;
+* ``numpy.random.default_rng(seed)``; per Gaussian the draws are centre
+  (d draws of U(0.1, 0.9)), width, amplitude; i.i.d. U(-1, 1) noise is drawn
+  after all Gaussians;
+* Gaussian a * exp(-|x-c|^2 / (2 w^2)), evaluated separably as the product of
+  per-axis exponentials (inputs only have to be identical for the oracle and the
+  GPU, which both consume the same arrays).
+
+Coefficients are returned as zero-stride broadcast views (``np.broadcast_to``)
+so a 32768^2 problem costs no coefficient memory; the GPU boundary detects the
+constant stencil and uses the scalar kernels.
+"""
+
+import math
+
+import numpy as np
+
+__all__ = ["CONFIGS", "gaussian_sum", "poisson_fields", "nonlinear_fields",
+           "config_fields"]
+
+# BASELINE.json configs -> (shape, P, table-N, source recipe)
+CONFIGS = {
+    "cfg1": dict(shape=(256, 256), p=2, n_table=256, n_gauss=8, noise=False,
+                 width=(0.02, 0.1), seed=1),
+    "cfg2": dict(shape=(4096, 4096), p=6, n_table=4096, n_gauss=8, noise=True,
+                 width=(0.02, 0.1), seed=2),
+    "cfg3": dict(shape=(512, 512, 512), p=10, n_table=512, n_gauss=16,
+                 noise=False, width=(0.02, 0.08), seed=3),
+    "cfg4": dict(shape=(32768, 32768), p=15, n_table=32768, n_gauss=32,
+                 noise=True, width=(0.02, 0.1), seed=4),
+    "cfg5": dict(shape=(256, 256, 256), p=8, n_table=256, nonlinear=True,
+                 seed=5),
+}
+
+
+def _axes(shape):
+    return [np.arange(1, n + 1, dtype=np.float64) / (n + 1) for n in shape]
+
+
+def gaussian_sum(shape, rng, n_gauss, width, amp=(-1.0, 1.0), peak=None):
+    """Sum of seeded Gaussians on the vertex-centred interior grid."""
+    nd = len(shape)
+    axes = _axes(shape)
+    out = np.zeros(shape)
+    for _ in range(n_gauss):
+        centre = rng.uniform(0.1, 0.9, nd)
+        w = rng.uniform(*width)
+        a = rng.uniform(*(peak if peak is not None else amp))
+        inv = 1.0 / (2.0 * w * w)
+        factors = [np.exp(-np.square(x - c) * inv) for x, c in zip(axes, centre)]
+        g = factors[0]
+        for f in factors[1:]:
+            g = np.multiply.outer(g, f)
+        out += a * g
+    return out
+
+
+def _stencil(shape):
+    h = [1.0 / (n + 1) for n in shape]
+    inv = [1.0 / (x * x) for x in h]
+    center = 0.0
+    for v in inv:
+        center += 2.0 * v
+    return (np.broadcast_to(np.float64(center), shape),
+            tuple(np.broadcast_to(np.float64(-v), shape) for v in inv),
+            tuple(np.broadcast_to(np.float64(-v), shape) for v in inv))
+
+
+def poisson_fields(shape, n_gauss=8, seed=1, noise=False, width=(0.02, 0.1)):
+    """Dirichlet Poisson Laplace(u)=f, u=0 on the boundary, u0=0.
+
+    Returns a dict with the reference GridProblem's fields (``u`` ghosted,
+    ``source`` = -f, ``center``, ``lower``, ``upper``, ``mask`` = None).
+    """
+    shape = tuple(int(n) for n in shape)
+    rng = np.random.default_rng(seed)
+    f = gaussian_sum(shape, rng, n_gauss, width)
+    if noise:
+        f += rng.uniform(-1.0, 1.0, shape)
+    center, lower, upper = _stencil(shape)
+    return {
+        "u": np.zeros(tuple(n + 2 for n in shape)),
+        "source": -f,
+        "center": center,
+        "lower": lower,
+        "upper": upper,
+        "mask": None,
+    }
+
+
+def nonlinear_fields(shape, seed=5, n_gauss=4):
+    """cfg5: -Laplace(psi) = 2 pi rho psi^5, psi = 1 on the boundary, psi0 = 1.
+
+    ``kappa`` = 2*pi*rho is the per-cell factor of the fused source
+    s(psi) = kappa * psi^5.
+    """
+    shape = tuple(int(n) for n in shape)
+    rng = np.random.default_rng(seed)
+    rho = gaussian_sum(shape, rng, n_gauss, width=(0.05, 0.15),
+                       peak=(0.01, 0.1))
+    center, lower, upper = _stencil(shape)
+    return {
+        "u": np.ones(tuple(n + 2 for n in shape)),
+        "source": np.zeros(shape),
+        "kappa": (2.0 * math.pi) * rho,
+        "center": center,
+        "lower": lower,
+        "upper": upper,
+        "mask": None,
+    }
+
+
+def config_fields(name, shape=None):
+    """Fields for a named BASELINE config, optionally at a reduced shape."""
+    cfg = CONFIGS[name]
+    shape = tuple(shape or cfg["shape"])
+    if cfg.get("nonlinear"):
+        return nonlinear_fields(shape, seed=cfg["seed"])
+    return poisson_fields(shape, cfg["n_gauss"], cfg["seed"], cfg["noise"],
+                          cfg["width"])

@@ -1,0 +1,126 @@
+"""Host-side behaviour of the drop-in API that needs no GPU.
+
+Mirrors the reference's validation tests (test_grids.py:123-250) against this
+package's GridProblem, and checks that the product path fails loudly -- never
+silently computes on the CPU -- when no CUDA device is present.
+"""
+
+import numpy as np
+import pytest
+
+from paper_1511_04292_b200 import grids as G
+from paper_1511_04292_b200.engine import constant_value
+
+
+def line_problem(bc, n=4):
+    u = np.zeros(n + 2)
+    u[1:-1] = 10.0 * (1.0 + np.arange(n))
+    return G.GridProblem(spacing=(1.0,), u=u, source=np.zeros(n),
+                         center=np.full(n, 2.0), lower=(np.full(n, -1.0),),
+                         upper=(np.full(n, -1.0),), bc=(bc,))
+
+
+def test_boundary_rules():
+    with pytest.raises(ValueError, match="boundary kind"):
+        G.BoundaryRule("absorbing")
+    with pytest.raises(ValueError, match="values"):
+        G.BoundaryRule("face_dirichlet")
+    with pytest.raises(ValueError, match="periodic"):
+        line_problem((G.PERIODIC, G.MIRROR))
+    p = line_problem((G.MIRROR, G.MIRROR))
+    assert p.u[0] == p.u[1] and p.u[-1] == p.u[-2]
+    p = line_problem((G.PERIODIC, G.PERIODIC))
+    assert p.u[0] == p.u[-2] and p.u[-1] == p.u[1]
+    p = line_problem((G.face_dirichlet(7.0), G.face_dirichlet(-1.0)))
+    assert p.u[0] == 2 * 7.0 - p.u[1] and p.u[-1] == 2 * (-1.0) - p.u[-2]
+    p = line_problem((G.FIXED, G.FIXED))
+    p.u[0], p.u[-1] = 123.0, 456.0
+    p.refresh_ghosts()
+    assert p.u[0] == 123.0 and p.u[-1] == 456.0
+
+
+def _kw(shape, **over):
+    one = np.ones(shape)
+    kw = dict(spacing=(1.0,) * len(shape), u=np.zeros(tuple(s + 2 for s in shape)),
+              source=np.zeros(shape), center=one, lower=(one,) * len(shape),
+              upper=(one,) * len(shape), bc=((G.FIXED, G.FIXED),) * len(shape))
+    kw.update(over)
+    return kw
+
+
+@pytest.mark.parametrize("over,match", [
+    (dict(u=np.zeros(4)), "ghost"),
+    (dict(spacing=(1.0, 1.0)), "spacing"),
+    (dict(lower=(np.ones(5),)), "neighbor"),
+    (dict(center=np.array([1.0, 1.0, 0.0, 1.0])), "center"),
+    (dict(mask=np.ones(5, dtype=bool)), "mask"),
+])
+def test_problem_validation(over, match):
+    with pytest.raises(ValueError, match=match):
+        G.GridProblem(**_kw((4,), **over))
+
+
+def test_four_dimensional_rejected():
+    with pytest.raises(ValueError, match="dimensional"):
+        G.GridProblem(**_kw((3, 3, 3, 3)))
+
+
+def test_zero_center_allowed_under_mask():
+    c = np.ones(4)
+    c[0] = 0.0
+    p = G.GridProblem(**_kw((4,), center=c, mask=np.array([False, True, True, True])))
+    assert p.shape == (4,)
+
+
+def test_residual_history_csv(tmp_path):
+    h = G.ResidualHistory(residual_inf=np.array([1.0, 0.5]),
+                          true_residual_inf=np.array([2.0, 1.0]),
+                          seconds=np.array([0.1, 0.2]), tolerance=1e-3,
+                          converged=False)
+    path = tmp_path / "h.csv"
+    h.to_csv(path)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "iteration,residual_inf,wall_seconds"
+    assert lines[1] == "1,1,0.100000" and len(lines) == 3
+    h.to_csv(path, timing=False)
+    assert path.read_text().endswith(",0.000000\n")
+
+
+def test_constant_detection_is_bitwise():
+    assert constant_value(np.broadcast_to(3.5, (4, 4))) == 3.5
+    a = np.full((3, 3), 2.0)
+    assert constant_value(a) == 2.0
+    a[1, 1] = -0.0 + 2.0 * (1 + 2 ** -52)
+    assert constant_value(a) is None
+    z = np.zeros((2, 2))
+    z[0, 0] = -0.0
+    assert constant_value(z) is None  # -0.0 and +0.0 differ in bits
+
+
+def test_argument_errors_precede_device_use():
+    p = G.GridProblem(**_kw((4, 4)))
+    with pytest.raises(ValueError, match="traversal"):
+        G.weighted_jacobi_sweep(p, 1.0, traversal="up")
+    with pytest.raises(ValueError, match="SOR"):
+        G.sor_solve(p, 2.5, 1e-6)
+
+
+def test_unsupported_features_raise():
+    p = G.GridProblem(**_kw((4,)))
+    with pytest.raises(NotImplementedError):
+        G.srj_solve(p, type("C", (), {"weight_sequence": np.ones(1)})(), 1e-6)
+    q = G.GridProblem(**_kw((4, 4), bc=((G.MIRROR, G.MIRROR),) * 2))
+    with pytest.raises(NotImplementedError):
+        G.jacobi_solve(q, 1e-6)
+    with pytest.raises(NotImplementedError):
+        G.gauss_seidel_solve(q, 1e-6)
+
+
+def test_no_cpu_fallback_without_cuda():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present; the GPU tests cover the device path")
+    p = G.GridProblem(**_kw((8, 8)))
+    with pytest.raises(RuntimeError, match="CUDA"):
+        G.jacobi_solve(p, 1e-6)

@@ -1,0 +1,112 @@
+"""Pin the CPU oracle against the reference's own outputs (tests/golden).
+
+The fixtures were produced by running the reference package
+(/root/reference/pkg/src/srj) with tools/make_golden.py; the oracle must
+reproduce them bit for bit, which is what makes it a valid checker for the GPU
+path on a machine where the reference is absent.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import fields_from, load_golden
+from helpers import problem_from
+
+FIXED_STEP_CASES = ["var2d", "var2d_mask", "var3d", "var3d_mask", "const2d_p6",
+                    "const3d_p6"]
+
+
+@pytest.mark.parametrize("name", FIXED_STEP_CASES)
+def test_oracle_reproduces_reference_steps(name):
+    g = load_golden(name)
+    p = problem_from(fields_from(g))
+    w = g["weights"]
+    steps = int(g["steps"])
+    done, status, norms = oracle.run(p, w, 0, steps)
+    assert done == steps and status == 0
+    assert np.array_equal(p.u, g["u_final"])
+    metric = norms[:, 0] / np.abs(w[np.arange(steps) % len(w)])
+    assert np.array_equal(metric, g["residual_inf"])
+    assert np.array_equal(norms[:, 1], g["true_residual_inf"])
+
+
+@pytest.mark.parametrize("name", ["var2d_mask", "var3d", "const2d_p6"])
+def test_numpy_restatement_matches_c_oracle(name):
+    g = load_golden(name)
+    a = problem_from(fields_from(g))
+    b = problem_from(fields_from(g))
+    for w in g["weights"][:25]:
+        assert oracle.step(a, w) == oracle.np_step(b, w)
+    assert np.array_equal(a.u, b.u)
+
+
+def test_oracle_threads_are_bitwise_neutral():
+    g = load_golden("var3d_mask")
+    a = problem_from(fields_from(g))
+    b = problem_from(fields_from(g))
+    _, _, na = oracle.run(a, g["weights"], 0, 40, nthreads=1)
+    _, _, nb = oracle.run(b, g["weights"], 0, 40, nthreads=4)
+    assert np.array_equal(a.u, b.u) and np.array_equal(na, nb)
+
+
+def test_oracle_reference_stopping_rule():
+    g = load_golden("solve2d_p2")
+    p = problem_from(fields_from(g))
+    steps, status, norms, _ = oracle.solve(p, g["weights"], float(g["tol"]))
+    assert status == 1 and bool(g["converged"])
+    assert steps == len(g["residual_inf"])
+    assert np.array_equal(p.u, g["u_final"])
+    metric = norms[:, 0] / np.abs(g["weights"][np.arange(steps) % len(g["weights"])])
+    assert np.array_equal(metric, g["residual_inf"])
+
+
+def test_oracle_divergence_guard():
+    g = load_golden("diverge2d")
+    p = problem_from(fields_from(g))
+    steps, status, norms = oracle.run(p, g["weights"], 0, 100_000, 1e-12)
+    assert status == 2
+    assert steps == int(g["iterations"])
+    metric = norms[:, 0] / np.abs(g["weights"][np.arange(steps) % len(g["weights"])])
+    assert np.array_equal(metric, g["residual_inf"])
+    assert np.array_equal(norms[:, 1], g["true_residual_inf"])
+
+
+def test_oracle_five_point_known_answers():
+    # test_grids.py:254-264: 5-point average 2.5; (dmax, rmax) = (1.25, 10.0)
+    g = load_golden("five_point")
+    for omega in (1.0, 0.5):
+        p = problem_from(fields_from(g))
+        dm, rm = oracle.step(p, omega)
+        want = g[f"w{omega}"]
+        assert (dm, rm, p.u[1, 1]) == tuple(want)
+    assert tuple(g["w1.0"])[2] == 2.5
+    assert tuple(g["w0.5"])[:2] == (1.25, 10.0)
+
+
+def test_oracle_residual_matches_numpy():
+    g = load_golden("var2d_mask")
+    p = problem_from(fields_from(g))
+    ss, mx = oracle.residual(p)
+    r = p.residual_field()[p.mask]
+    assert mx == np.max(np.abs(r))
+    assert ss == pytest.approx(float(np.sum(r * r)), rel=1e-13)
+
+
+def test_oracle_nonlinear_source_restatement():
+    from paper_1511_04292_b200.problems import nonlinear_fields
+    from paper_1511_04292_b200.schedule import quantize
+    from paper_1511_04292_b200.tables import shipped_table
+
+    f = nonlinear_fields((30, 32, 34), seed=5)
+    w = quantize(shipped_table().get(8, 32)).weight_sequence
+    a = problem_from(f)
+    b = problem_from(f)
+    for k in range(30):
+        assert oracle.step(a, w[k], kappa=f["kappa"]) == oracle.np_step(b, w[k], kappa=f["kappa"])
+    assert np.array_equal(a.u, b.u)
+    # the nonlinear residual decreases over a cycle of the P=6 schedule
+    r0 = oracle.residual(problem_from(f), kappa=f["kappa"])[0]
+    c = problem_from(f)
+    oracle.run(c, w, 0, len(w), kappa=f["kappa"])
+    assert oracle.residual(c, kappa=f["kappa"])[0] < r0

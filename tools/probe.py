@@ -1,0 +1,76 @@
+"""Quick throughput probe of the sweep kernels (development tool, not the bench).
+
+python tools/probe.py [--n 4096] [--fuse 1,2,4,8] [--steps 400]
+Prints GLUPS and the algorithmic-HBM fraction (24 B per point-update) for the
+2D kernel at each fused depth and the 3D kernel at 512^3 / 256^3.
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_1511_04292_b200.engine import DeviceGrid  # noqa: E402
+from paper_1511_04292_b200.problems import config_fields  # noqa: E402
+from paper_1511_04292_b200.schedule import quantize  # noqa: E402
+from paper_1511_04292_b200.tables import shipped_table  # noqa: E402
+
+PEAK = 6555.5
+
+
+def measure(f, w, steps, fuse, warm=2):
+    dev = DeviceGrid(f["u"], f["source"], f["center"], f["lower"], f["upper"],
+                     kappa=f.get("kappa"))
+    cells = int(np.prod(f["source"].shape))
+    cur = 0
+    for _ in range(warm):
+        cur = dev.run(cur, w, 0, min(steps, 64), fuse)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(dev.stream)
+    cur = dev.run(cur, w, 0, steps, fuse)
+    e1.record(dev.stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    glups = cells * steps / (ms * 1e-3) / 1e9
+    dev.close()
+    return ms / steps, glups, glups * 24 / PEAK
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--fuse", default="1,2,3,4,5,6,8")
+    ap.add_argument("--steps", type=int, default=480)
+    ap.add_argument("--three", default="512,256")
+    a = ap.parse_args()
+    tab = shipped_table()
+    w = quantize(tab.lookup(6, 4096)).weight_sequence
+    f = config_fields("cfg2", (a.n, a.n))
+    out = []
+    for fuse in [int(x) for x in a.fuse.split(",") if x]:
+        ms, g, frac = measure(f, w, a.steps, fuse)
+        r = dict(kind="2d", n=a.n, fuse=fuse, ms_per_sweep=ms, glups=g, frac_alg=frac)
+        print(json.dumps(r), flush=True)
+        out.append(r)
+    for n in [int(x) for x in a.three.split(",") if x]:
+        f3 = config_fields("cfg3", (n, n, n))
+        w3 = quantize(tab.lookup(10, 512)).weight_sequence
+        ms, g, frac = measure(f3, w3, 40, 1)
+        print(json.dumps(dict(kind="3d", n=n, ms_per_sweep=ms, glups=g, frac_alg=frac)), flush=True)
+    f5 = config_fields("cfg5", (256, 256, 256))
+    w5 = quantize(tab.lookup(8, 256)).weight_sequence
+    ms, g, frac = measure(f5, w5, 40, 1)
+    print(json.dumps(dict(kind="3d-nl", n=256, ms_per_sweep=ms, glups=g, frac_alg=frac)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
