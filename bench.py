@@ -1,0 +1,350 @@
+"""Benchmark: SRJ point-updates/s (GLUPS) on the BASELINE cfg2 workload.
+
+Workload (BASELINE.json configs[1]): 2D Poisson, 4096 x 4096 interior, fp64,
+Dirichlet u=0, 5-point stencil, f = i.i.d. U(-1,1) + 8 seeded Gaussians,
+SRJ P=6 schedule (table row N=4096, M=25,530 sweeps per cycle).  One bench
+"step" is one full M-cycle (25,530 sweeps) including the per-step
+(dmax, rmax) norms and the host-side stopping-rule check of the cycle's norm
+buffer.  Fields are 134 MB each (u, u_next, f = 403 MB > 126 MB L2), so every
+sweep streams from HBM: no L2 flush is needed.
+
+value  : GLUPS with the inputs resident in HBM (device-timed, CUDA events).
+e2e    : GLUPS through the public API ``srj_solve`` with pinned host arrays;
+         each call uploads u and f, runs one cycle, downloads u.
+roofline: dominant kernel = fused 2D band sweep; algorithmic bytes = 24 B per
+         point-update (read u, read f, write u_next) x T fused sweeps.
+cpu_baseline: the oracle port (oracle/srj_oracle.c, the reference's _wj2
+         arithmetic) on the host cores, on a bounded sample of sweeps.
+
+N > 1 (torchrun): weak scaling -- every rank owns a 4096 x 4096 row block of a
+(4096 N) x 4096 grid, exchanging one halo block per fused launch
+(distributed.py).  ``--impl reference`` times the CPU oracle port instead.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+BYTES_PER_UPDATE = 24.0
+WORKLOAD = "cfg2"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return PEAKS_FALLBACK["hbm_gbs"], "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def schedule():
+    from paper_1511_04292_b200.schedule import quantize
+    from paper_1511_04292_b200.tables import shipped_table
+
+    ws = shipped_table().lookup(6, 4096)
+    return ws, quantize(ws)
+
+
+def cpu_baseline(fields, weights, budget_s=12.0, max_sweeps=4096, threads=None):
+    """Oracle port (reference _wj2 arithmetic) on the host: GLUPS on a sample."""
+    import oracle
+
+    from paper_1511_04292_b200.grids import FIXED, GridProblem
+
+    threads = threads or os.cpu_count() or 1
+    p = GridProblem(spacing=(1.0, 1.0), u=fields["u"].copy(), source=fields["source"],
+                    center=np.ascontiguousarray(fields["center"]),
+                    lower=tuple(np.ascontiguousarray(a) for a in fields["lower"]),
+                    upper=tuple(np.ascontiguousarray(a) for a in fields["upper"]),
+                    bc=((FIXED, FIXED),) * 2)
+    cells = int(np.prod(p.shape))
+    oracle.run(p, weights, 0, 1, nthreads=threads)  # warm (page-in, threads)
+    done, t0 = 0, time.perf_counter()
+    while done < max_sweeps and time.perf_counter() - t0 < budget_s:
+        oracle.run(p, weights, 1 + done, 4, nthreads=threads)
+        done += 4
+    dt = time.perf_counter() - t0
+    return {"value": cells * done / dt / 1e9, "unit": "GLUPS", "cores": threads,
+            "kind": "port",
+            "sample": f"{done} sweeps of the cfg2 schedule on the full 4096^2 grid "
+                      f"(oracle/srj_oracle.c, reference _wj2 arithmetic, per-cell "
+                      f"coefficient arrays as the reference stores them), {dt:.1f} s"}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1511_04292_b200.problems import config_fields
+
+    _, cyc = schedule()
+    f = config_fields(WORKLOAD)
+    threads = os.cpu_count() or 1
+    import oracle
+    from paper_1511_04292_b200.grids import FIXED, GridProblem
+
+    p = GridProblem(spacing=(1.0, 1.0), u=f["u"].copy(), source=f["source"],
+                    center=np.ascontiguousarray(f["center"]),
+                    lower=tuple(np.ascontiguousarray(a) for a in f["lower"]),
+                    upper=tuple(np.ascontiguousarray(a) for a in f["upper"]),
+                    bc=((FIXED, FIXED),) * 2)
+    cells = int(np.prod(p.shape))
+    w = cyc.weight_sequence
+    sweeps_per_step = 8
+    k = 0
+    for _ in range(args.warmup):
+        oracle.run(p, w, k, sweeps_per_step, nthreads=threads)
+        k += sweeps_per_step
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.run(p, w, k, sweeps_per_step, nthreads=threads)
+        k += sweeps_per_step
+    dt = time.perf_counter() - t0
+    v = cells * sweeps_per_step * args.steps / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "grid-point updates/sec (GLUPS) fp64",
+        "value": v, "unit": "GLUPS", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: 2D Poisson 4096^2, P=6 SRJ (N=4096 row, M=25530)",
+                   "step": f"{sweeps_per_step} sweeps (bounded CPU sample of one cycle)"},
+        "cpu_baseline": {"value": v, "unit": "GLUPS", "cores": threads, "kind": "port",
+                         "sample": f"{sweeps_per_step} sweeps x {args.steps} steps of cfg2 "
+                                   "on the full grid, oracle/srj_oracle.c (OpenMP rows)"},
+        "e2e": {"value": v, "unit": "GLUPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1511_04292_b200 import grids as G
+    from paper_1511_04292_b200.problems import config_fields
+
+    _, cyc = schedule()
+    w = cyc.weight_sequence
+    m = cyc.m
+    base = config_fields(WORKLOAD)
+    n0, n1 = base["source"].shape
+    fuse = args.fuse
+    if ws > 1:
+        from paper_1511_04292_b200.distributed import SlabGrid
+
+        grid = SlabGrid.weak_rows(base, rank, ws, fuse=fuse or 4)
+        cells_rank = grid.owned_cells
+    else:
+        from paper_1511_04292_b200.engine import DeviceGrid
+
+        grid = DeviceGrid(base["u"], base["source"], base["center"], base["lower"],
+                          base["upper"])
+        cells_rank = n0 * n1
+    total_cells = cells_rank * ws
+    stream = grid.stream
+    from paper_1511_04292_b200 import _lib
+
+    T = fuse or 4
+    launches_per_cycle = -(-m // T)
+
+    def one_cycle(cur, first):
+        out = grid.run(cur, w, first, m, fuse)
+        norms = grid.norms[:2 * m].view(m, 2).cpu().numpy()  # the per-cycle host check
+        metric = norms[:, 0] / np.abs(w)
+        if not np.all(np.isfinite(metric)):
+            raise RuntimeError("non-finite update norm in benchmark cycle")
+        return out
+
+    cur = 0
+    k = 0
+    for _ in range(args.warmup):
+        cur = one_cycle(cur, k)
+        k += m
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    cyc_ms = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            cur = one_cycle(cur, k)
+            b.record(stream)
+            k += m
+            cyc_ms.append((a, b))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    elapsed = ev0.elapsed_time(ev1)
+    kernel_ms = sum(a.elapsed_time(b) for a, b in cyc_ms)
+    if ws > 1:
+        t = torch.tensor([elapsed, kernel_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed, kernel_ms = float(t[0]), float(t[1])
+    value = total_cells * m * args.steps / (elapsed * 1e-3) / 1e9
+    avg_launch_ms = kernel_ms / (args.steps * launches_per_cycle)
+    peak, peak_kind = peaks()
+    achieved = cells_rank * T * BYTES_PER_UPDATE / (avg_launch_ms * 1e-3) / 1e9
+
+    e2e = None
+    cpu = None
+    if rank == 0 and ws == 1:
+        e2e = measure_e2e(G, base, cyc, args.e2e_steps)
+        if not args.no_cpu:
+            cpu = cpu_baseline(base, w)
+    if ws > 1:
+        torch.distributed.barrier()
+    if rank != 0:
+        return
+    line = {
+        "metric": "grid-point updates/sec (GLUPS) fp64",
+        "value": value, "unit": "GLUPS", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: 2D Poisson 4096^2 per GPU, P=6 SRJ schedule "
+                               "(table row N=4096, M=25530), fp64, 5-point, Dirichlet",
+                   "step": "one full M-cycle (25530 sweeps) + per-step norms + host check",
+                   "fuse": T, "l2": "inputs larger than L2 (3 x 134 MB streamed per sweep)",
+                   "parallelism": f"row-block x{ws}" if ws > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "peak_kind": peak_kind,
+                     "kernel": f"sweep2d_tb<T={T}> (fused {T} sweeps/launch)",
+                     "algorithmic_bytes_per_launch": cells_rank * T * BYTES_PER_UPDATE,
+                     "avg_launch_ms": avg_launch_ms},
+        "clocks": clk.summary(),
+        "gpu_launches": args.steps * launches_per_cycle,
+        "glups_per_gpu": value / ws,
+        "frac_of_hbm_roofline_single_sweep": value / ws * BYTES_PER_UPDATE / peak,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def measure_e2e(G, base, cyc, steps):
+    """srj_solve on pinned host arrays: h2d u+f, one cycle, d2h u, per call."""
+    import torch
+
+    n0, n1 = base["source"].shape
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    u = pin(base["u"])
+    src = pin(base["source"])
+    p = G.GridProblem(spacing=(1.0, 1.0), u=u, source=src, center=base["center"],
+                      lower=base["lower"], upper=base["upper"], bc=((G.FIXED, G.FIXED),) * 2)
+    m = cyc.m
+    G.srj_solve(p, cyc, tol=1e-300, max_iters=m)  # warm (allocator, page-in)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        hist, _ = G.srj_solve(p, cyc, tol=1e-300, max_iters=m)
+    dt = time.perf_counter() - t0
+    cells = n0 * n1
+    return {"value": cells * m * steps / dt / 1e9, "unit": "GLUPS",
+            "h2d_bytes_per_step": int(u.nbytes + src.nbytes),
+            "d2h_bytes_per_step": int(u.nbytes + 16 * m),
+            "calls": steps, "api": "paper_1511_04292_b200.srj_solve(problem, cycle, tol, max_iters=M)"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--fuse", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

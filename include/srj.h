@@ -164,6 +164,13 @@ int srj_copy_layers(const srj_layout_t *lay, const double *src,
                     int64_t src_layer, double *dst, int64_t dst_layer,
                     int64_t count, void *stream);
 
+/* Diagnostic: out[i] = a[i]/c through the reciprocal-refinement division the
+ * constant-stencil kernels use (y = RN(1/c), two Markstein corrections), and
+ * ref[i] = the IEEE-754 quotient; device arrays of n doubles.  Tests assert
+ * out == ref bit for bit. */
+int srj_selftest_div(const double *a, int64_t n, double c, double *out,
+                     double *ref, void *stream);
+
 int srj_abi_version(void);
 const char *srj_last_error(void);
 

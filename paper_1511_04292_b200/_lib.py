@@ -79,6 +79,8 @@ _SIGNATURES = {
                                           ctypes.c_void_p, ctypes.c_void_p]),
     "srj_upload_interior": (ctypes.c_int, [ctypes.POINTER(SrjLayout), ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]),
+    "srj_selftest_div": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "srj_copy_layers": (ctypes.c_int, [ctypes.POINTER(SrjLayout), ctypes.c_void_p,
                                        ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                        ctypes.c_int64, ctypes.c_void_p]),

@@ -47,6 +47,14 @@ int cuda_fail(cudaError_t e, const char *what) {
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// y = RN(1/c) for the reciprocal division path (srj_sweep2d.cuh div_by_const),
+// or 0 to keep the IEEE division when c is outside [2^-100, 2^100].
+double recip_or_zero(double c) {
+  const double a = c < 0 ? -c : c;
+  if (!(a >= 0x1p-100 && a <= 0x1p+100)) return 0.0;
+  return 1.0 / c;
+}
+
 // offset of interior cell (0,0[,0])
 int64_t interior_offset(const srj_layout_t &l) {
   return l.origin + int64_t(l.halo0) * l.plane + (l.ndim == 3 ? l.pitch : 0) + 1;
@@ -133,6 +141,15 @@ int blocks_per_sm_2d(int T) {
 
 }  // namespace
 
+__global__ void selftest_div(const double *a, int64_t n, double c, double y, double *out,
+                             double *ref) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    out[i] = y != 0.0 ? div_by_const(a[i], c, y) : __ddiv_rn(a[i], c);
+    ref[i] = __ddiv_rn(a[i], c);
+  }
+}
+
 struct srj_plan {
   srj_plan_desc d;
   int default_fuse;
@@ -142,6 +159,17 @@ struct srj_plan {
 extern "C" {
 
 int srj_abi_version(void) { return SRJ_ABI_VERSION; }
+
+int srj_selftest_div(const double *a, int64_t n, double c, double *out, double *ref,
+                     void *stream) {
+  if (!a || !out || !ref || n < 0) return fail(SRJ_EINVAL, "bad argument");
+  if (n == 0) return SRJ_OK;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(sm_count()) * 32));
+  selftest_div<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, n, c, recip_or_zero(c),
+                                                                       out, ref);
+  SRJ_CUDA(cudaGetLastError());
+  return SRJ_OK;
+}
 const char *srj_last_error(void) { return g_err; }
 int srj_max_fuse(void) { return kMaxFuse; }
 
@@ -313,6 +341,7 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.kap0 = d.coef[2];
       p.kam1 = d.coef[3];
       p.kap1 = d.coef[4];
+      p.kinv = recip_or_zero(d.coef[0]);
       p.pitch = l.pitch;
       p.n0 = int(l.n[0]);
       p.n1 = int(l.n[1]);

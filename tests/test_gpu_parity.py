@@ -247,3 +247,32 @@ def test_fusion_depth_invariance_full_size_cfg2(table):
         h, _ = run_steps(p, w, 48, fuse=fuse)
         assert np.array_equal(p.u, ref.u)
         assert np.array_equal(h.residual_inf, h1.residual_inf)
+
+
+@pytest.mark.parametrize("c", [67141636.00000001, 4.0 * 4097.0 ** 2, 6.0 * 513.0 ** 2,
+                               3.0, 7.123456789, -5.5, 1e-30, 2.0 ** 60 + 12345.0])
+def test_reciprocal_division_is_correctly_rounded(c):
+    """The constant-stencil kernels divide by c through y = RN(1/c) plus two
+    Markstein corrections; it must equal IEEE division bit for bit."""
+    import torch
+
+    from paper_1511_04292_b200 import _lib
+
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    n = 1 << 24
+    for lo, hi in ((-60.0, 60.0), (-1000.0, 1000.0), (-1.0, 1.0)):
+        mant = torch.rand(n, generator=g, device="cuda", dtype=torch.float64) + 1.0
+        expo = torch.randint(int(lo), int(hi), (n,), generator=g, device="cuda")
+        sign = torch.where(torch.rand(n, generator=g, device="cuda") < 0.5, -1.0, 1.0)
+        a = (sign * torch.ldexp(mant, expo)).to(torch.float64)
+        # adversarial mantissas near midpoints of quotients
+        a[: n // 4] = torch.nextafter(a[: n // 4] * c, torch.full_like(a[: n // 4], float("inf")))
+        a[:8] = torch.tensor([0.0, -0.0, float("inf"), -float("inf"), float("nan"),
+                              1e-310, -1e300, 5e-324], dtype=torch.float64)
+        out = torch.empty_like(a)
+        ref = torch.empty_like(a)
+        _lib.check(lib.srj_selftest_div(a.data_ptr(), n, c, out.data_ptr(), ref.data_ptr(), None))
+        torch.cuda.synchronize()
+        same = (out.view(torch.int64) == ref.view(torch.int64)) | (torch.isnan(out) & torch.isnan(ref))
+        assert bool(same.all()), f"{int((~same).sum())} mismatches for c={c}"

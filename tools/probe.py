@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--fuse", default="1,2,3,4,5,6,8")
     ap.add_argument("--steps", type=int, default=480)
     ap.add_argument("--three", default="512,256")
+    ap.add_argument("--nl", type=int, default=1)
     a = ap.parse_args()
     tab = shipped_table()
     w = quantize(tab.lookup(6, 4096)).weight_sequence
@@ -66,6 +67,8 @@ def main():
         w3 = quantize(tab.lookup(10, 512)).weight_sequence
         ms, g, frac = measure(f3, w3, 40, 1)
         print(json.dumps(dict(kind="3d", n=n, ms_per_sweep=ms, glups=g, frac_alg=frac)), flush=True)
+    if not a.nl:
+        return
     f5 = config_fields("cfg5", (256, 256, 256))
     w5 = quantize(tab.lookup(8, 256)).weight_sequence
     ms, g, frac = measure(f5, w5, 40, 1)
