@@ -50,8 +50,7 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 // y = RN(1/c) for the reciprocal division path (srj_sweep2d.cuh div_by_const),
 // or 0 to keep the IEEE division when c is outside [2^-100, 2^100].
 double recip_or_zero(double c) {
-  const double a = c < 0 ? -c : c;
-  if (!(a >= 0x1p-100 && a <= 0x1p+100)) return 0.0;
+  if (!(c >= 0x1p-100 && c <= 0x1p+100)) return 0.0;  // c > 0 only (div_recip sign rule)
   return 1.0 / c;
 }
 
@@ -72,71 +71,61 @@ int sm_count() {
 }
 
 // ------------------------------------------------------------ 2D dispatch
-using Sweep2DFn = void (*)(const Sweep2DParams &, int blocks, cudaStream_t);
+// One entry per kernel instantiation: launcher + resident blocks per SM
+// (registers and shared memory both counted, from the occupancy API), so the
+// launch can be sized to exactly one wave.
+struct Kernel2D {
+  void (*launch)(const Sweep2DParams &, int blocks, cudaStream_t);
+  int (*blocks_per_sm)();
+  int own;  // columns owned per band
+};
 
-template <int T, bool VAR, bool NL>
-void launch2d(const Sweep2DParams &p, int blocks, cudaStream_t s) {
+template <int T, bool VAR, bool NL, bool RECIP>
+struct K2 {
   using B = Band2D<T>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(sweep2d_tb<T, VAR, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(B::smem_bytes()));
-    configured = true;
+  static void configure() {
+    static bool done = false;
+    if (!done) {
+      cudaFuncSetAttribute(sweep2d_tb<T, VAR, NL, RECIP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(B::smem_bytes()));
+      done = true;
+    }
   }
-  sweep2d_tb<T, VAR, NL><<<blocks, B::WARPS * 32, B::smem_bytes(), s>>>(p);
-}
-
-template <bool VAR, bool NL>
-Sweep2DFn pick2d(int T) {
-  switch (T) {
-    case 1: return launch2d<1, VAR, NL>;
-    case 2: return launch2d<2, VAR, NL>;
-    case 3: return launch2d<3, VAR, NL>;
-    case 4: return launch2d<4, VAR, NL>;
-    case 5: return launch2d<5, VAR, NL>;
-    case 6: return launch2d<6, VAR, NL>;
-    case 7: return launch2d<7, VAR, NL>;
-    case 8: return launch2d<8, VAR, NL>;
+  static void launch(const Sweep2DParams &p, int blocks, cudaStream_t s) {
+    configure();
+    sweep2d_tb<T, VAR, NL, RECIP><<<blocks, B::WARPS * 32, B::smem_bytes(), s>>>(p);
   }
-  return nullptr;
-}
-
-Sweep2DFn pick2d(int T, bool var, bool nl) {
-  if (var) return nl ? pick2d<true, true>(T) : pick2d<true, false>(T);
-  return nl ? pick2d<false, true>(T) : pick2d<false, false>(T);
-}
+  static int bps() {
+    static int n = 0;
+    if (n == 0) {
+      configure();
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_tb<T, VAR, NL, RECIP>,
+                                                    B::WARPS * 32, B::smem_bytes());
+      if (n <= 0) n = 1;
+    }
+    return n;
+  }
+  static Kernel2D get() { return Kernel2D{launch, bps, B::OWN}; }
+};
 
 template <int T>
-int own_cols() { return Band2D<T>::OWN; }
-
-int band_own(int T) {
-  switch (T) {
-    case 1: return own_cols<1>();
-    case 2: return own_cols<2>();
-    case 3: return own_cols<3>();
-    case 4: return own_cols<4>();
-    case 5: return own_cols<5>();
-    case 6: return own_cols<6>();
-    case 7: return own_cols<7>();
-    default: return own_cols<8>();
-  }
+Kernel2D pick2d_t(bool var, bool nl, bool recip) {
+  if (var) return nl ? K2<T, true, true, false>::get() : K2<T, true, false, false>::get();
+  if (recip) return nl ? K2<T, false, true, true>::get() : K2<T, false, false, true>::get();
+  return nl ? K2<T, false, true, false>::get() : K2<T, false, false, false>::get();
 }
 
-int blocks_per_sm_2d(int T) {
-  // shared-memory bound occupancy of the band kernel (4 warps per block)
-  size_t bytes = 0;
+Kernel2D pick2d(int T, bool var, bool nl, bool recip) {
   switch (T) {
-    case 1: bytes = Band2D<1>::smem_bytes(); break;
-    case 2: bytes = Band2D<2>::smem_bytes(); break;
-    case 3: bytes = Band2D<3>::smem_bytes(); break;
-    case 4: bytes = Band2D<4>::smem_bytes(); break;
-    case 5: bytes = Band2D<5>::smem_bytes(); break;
-    case 6: bytes = Band2D<6>::smem_bytes(); break;
-    case 7: bytes = Band2D<7>::smem_bytes(); break;
-    default: bytes = Band2D<8>::smem_bytes(); break;
+    case 1: return pick2d_t<1>(var, nl, recip);
+    case 2: return pick2d_t<2>(var, nl, recip);
+    case 3: return pick2d_t<3>(var, nl, recip);
+    case 4: return pick2d_t<4>(var, nl, recip);
+    case 5: return pick2d_t<5>(var, nl, recip);
+    case 6: return pick2d_t<6>(var, nl, recip);
+    case 7: return pick2d_t<7>(var, nl, recip);
+    default: return pick2d_t<8>(var, nl, recip);
   }
-  int b = int((227 * 1024) / (bytes + 1024));
-  return std::max(1, std::min(b, 8));
 }
 
 }  // namespace
@@ -145,7 +134,12 @@ __global__ void selftest_div(const double *a, int64_t n, double c, double y, dou
                              double *ref) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
-    out[i] = y != 0.0 ? div_by_const(a[i], c, y) : __ddiv_rn(a[i], c);
+    double q = __ddiv_rn(a[i], c);
+    if (y != 0.0) {  // exactly what the RECIP sweep kernels compute
+      q = div_recip(a[i], c, y);
+      if (recip_unsafe(a[i])) q = div_ieee(a[i], c);
+    }
+    out[i] = q;
     ref[i] = __ddiv_rn(a[i], c);
   }
 }
@@ -351,10 +345,11 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.ld_hi = ld_hi;
       p.own_b = int(d.own0_begin);
       p.own_e = int(d.own0_end);
-      const int own = band_own(t);
-      p.nbands = int((l.n[1] + own - 1) / own);
-      const int target = sm_count() * blocks_per_sm_2d(t) * Band2D<1>::WARPS;
-      int nstrips = std::max(1, (target + p.nbands / 2) / p.nbands);
+      const Kernel2D k2 = pick2d(t, var, nl, !var && p.kinv != 0.0);
+      p.nbands = int((l.n[1] + k2.own - 1) / k2.own);
+      // exactly one wave: strips x bands <= resident warps
+      const int capacity = sm_count() * k2.blocks_per_sm() * Band2D<1>::WARPS;
+      int nstrips = std::max(1, capacity / p.nbands);
       nstrips = std::min(nstrips, std::max(1, rows / std::max(2 * t, 8)));
       p.H = (rows + nstrips - 1) / nstrips;
       p.nstrips = (rows + p.H - 1) / p.H;
@@ -362,7 +357,7 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.norms = d_norms + 2 * k;
       const int warps = p.nbands * p.nstrips;
       const int blocks = (warps + Band2D<1>::WARPS - 1) / Band2D<1>::WARPS;
-      pick2d(t, var, nl)(p, blocks, st);
+      k2.launch(p, blocks, st);
     } else {
       Sweep3DParams p{};
       p.src = cur + ioff;

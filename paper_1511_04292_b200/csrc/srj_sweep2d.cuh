@@ -20,8 +20,9 @@
 //    |RN(RN(omega*r)/c)| is a monotone function of |r|, so
 //    max|d| = |RN(RN(omega*max|r|)/c)| exactly (evaluated once per warp);
 //  * with a constant stencil the division uses a precomputed y = RN(1/c) and
-//    two Markstein corrections (correctly rounded, see div_by_const), with the
-//    IEEE division kept for zero/inf/NaN and extreme exponents.
+//    two Markstein corrections, branch-free (correctly rounded, div_recip);
+//    one warp vote per stage sends the rare subnormal/huge/inf/NaN
+//    numerators to the IEEE division.
 //
 // Bitwise contract: the arithmetic per cell and step is exactly the reference
 // _wj2 (grids.py:351-376); ghost rows/columns and inactive (masked) cells pass
@@ -65,27 +66,35 @@ struct Band2D {
   }
 };
 
-// RN(a/c) for a fixed divisor c with y = RN(1/c): q0 = RN(a*y) is within
-// 1.5 ulp; one Markstein correction q1 = RN(q0 + RN(a - c*q0)*y) brings it
-// within 1 ulp; with q1 faithful and y within 1/2 ulp of 1/c, Markstein's
-// theorem makes r1 = a - c*q1 exact and RN(q1 + r1*y) = RN(a/c).  The range
-// guard keeps a, a/c and the remainders away from overflow/underflow, and
-// sends 0 (sign of zero), inf and NaN to the IEEE division.
+// RN(a/c) for a fixed divisor c > 0 with y = RN(1/c), branch-free:
+// q0 = RN(a*y) is within 1.5 ulp of a/c; one Markstein correction
+// q1 = RN(q0 + RN(a - c*q0)*y) brings it within 1 ulp; with q1 faithful and y
+// within 1/2 ulp of 1/c, Markstein's theorem makes r1 = a - c*q1 exact and
+// RN(q1 + r1*y) = RN(a/c).  The sign is copied from a, which is exact for
+// c > 0 and restores IEEE's -0/c = -0.  Valid for a = +-0 and for normal a
+// with exponent in [-899, 899] (no overflow/underflow in q, r); other inputs
+// (subnormal, huge, inf, NaN) are flagged by recip_unsafe() and redone with
+// the IEEE division after a warp vote (see stage2d).
+__device__ __forceinline__ double div_recip(double a, double c, double y) {
+  double q = __dmul_rn(a, y);
+  double r = __fma_rn(-q, c, a);
+  q = __fma_rn(r, y, q);
+  r = __fma_rn(-q, c, a);
+  q = __fma_rn(r, y, q);
+  const int hi = (__double2hiint(q) & 0x7fffffff) | (__double2hiint(a) & int(0x80000000));
+  return __hiloint2double(hi, __double2loint(q));
+}
+
+__device__ __forceinline__ bool recip_unsafe(double a) {
+  const unsigned hi = unsigned(__double2hiint(a)) & 0x7fffffffu;
+  const unsigned e = hi >> 20;
+  const bool zero = (hi | unsigned(__double2loint(a))) == 0u;
+  return (e - 124u > 1798u) && !zero;  // exponent outside [-899, 899], nonzero
+}
+
 // out of line: the IEEE division is the rare path and its inline expansion
 // would triple the size of the unrolled fast loop
 __device__ __noinline__ double div_ieee(double a, double c) { return __ddiv_rn(a, c); }
-
-__device__ __forceinline__ double div_by_const(double a, double c, double y) {
-  const double aa = fabs(a);
-  if (aa > 0x1p-900 && aa < 0x1p+900) {
-    double q = __dmul_rn(a, y);
-    double r = __fma_rn(-q, c, a);
-    q = __fma_rn(r, y, q);
-    r = __fma_rn(-q, c, a);
-    return __fma_rn(r, y, q);
-  }
-  return div_ieee(a, c);
-}
 
 // keep the entry of larger magnitude (signed); NaN never replaces m
 __device__ __forceinline__ void acc_absmax(double &m, double x) {
@@ -95,11 +104,11 @@ __device__ __forceinline__ void acc_absmax(double &m, double x) {
 // One stage of the fused pipeline for the lane's V cells: the window rows
 // (up, mid) hold stage t-1 rows r-1, r; x arrives holding row r+1 and leaves
 // holding the stage-t value of row r.
-template <bool FAST, bool VAR, bool NL, int V, int S, int BAND>
+template <bool FAST, bool VAR, bool NL, bool RECIP, int V, int S, int BAND>
 __device__ __forceinline__ void stage2d(const Sweep2DParams &p, double (&up)[V], double (&mid)[V],
                                         double (&down)[V], double (&x)[V],
                                         const double *ring_f, int fslot, int lane, int r,
-                                        double om, bool use_recip, int lane_col, int i0, int i1,
+                                        double om, int lane_col, int i0, int i1,
                                         int own_c0, int own_c1, int f_lo, int f_hi, double &rmx,
                                         double &dmx) {
 #pragma unroll
@@ -121,6 +130,8 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, double (&up)[V],
     row_own = (r >= i0) && (r < i1);
     rc = min(max(r, f_lo), f_hi);
   }
+  double num[V], cv[V];
+  bool actv[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const double uc = mid[v];
@@ -143,22 +154,47 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, double (&up)[V],
     }
     const double s = NL ? nl_source(fv[v], uc) : fv[v];
     const double rr = resid5(s, c, uc, a0, up[v], b0, down[v], a1, uw, b1, ue);
-    const double num = __dmul_rn(om, rr);
-    const double d = use_recip ? div_by_const(num, c, p.kinv) : __ddiv_rn(num, c);
+    num[v] = __dmul_rn(om, rr);
+    if (!FAST && !act) num[v] = 0.0;  // passthrough cell: keep garbage off the slow path
+    cv[v] = c;
+    actv[v] = act;
     if (FAST) {
-      x[v] = __dadd_rn(uc, d);
       acc_absmax(rmx, rr);
+    } else if (act && (r >= i0) && (r < i1) && col >= own_c0 && col < own_c1) {
+      acc_absmax(rmx, rr);
+    }
+  }
+  double d[V];
+  if (RECIP) {
+    bool bad = false;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      d[v] = div_recip(num[v], p.kc, p.kinv);
+      bad |= recip_unsafe(num[v]);
+    }
+    if (__any_sync(kFull, bad)) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (recip_unsafe(num[v])) d[v] = div_ieee(num[v], p.kc);
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) d[v] = __ddiv_rn(num[v], cv[v]);
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double uc = mid[v];
+    if (FAST) {
+      x[v] = __dadd_rn(uc, d[v]);
     } else {
-      x[v] = act ? __dadd_rn(uc, d) : uc;
-      if (act && row_own && col >= own_c0 && col < own_c1) {
-        acc_absmax(rmx, rr);
-        if (VAR) acc_absmax(dmx, d);
-      }
+      x[v] = actv[v] ? __dadd_rn(uc, d[v]) : uc;
+      if (VAR && actv[v] && row_own && lane_col + v >= own_c0 && lane_col + v < own_c1)
+        acc_absmax(dmx, d[v]);
     }
   }
 }
 
-template <int T, bool VAR, bool NL>
+template <int T, bool VAR, bool NL, bool RECIP>
 __global__ void __launch_bounds__(Band2D<T>::WARPS * 32)
     sweep2d_tb(const __grid_constant__ Sweep2DParams p) {
   using B = Band2D<T>;
@@ -191,7 +227,6 @@ __global__ void __launch_bounds__(Band2D<T>::WARPS * 32)
   const int fast_hi = min(i1, p.hi_c);         // rho - 1 < fast_hi
   const int lane_col = col_band + V * lane;
   const bool lane_owned = (lane_col >= own_c0) && (lane_col + V <= own_c1);
-  const bool use_recip = !VAR && p.kinv != 0.0;
 
   auto issue = [&](int slot, int tick) {
     const int r = rho_b + tick;
@@ -245,17 +280,17 @@ __global__ void __launch_bounds__(Band2D<T>::WARPS * 32)
       if (band_interior && rho >= fast_lo && rho <= fast_hi) {
 #pragma unroll
         for (int t = 1; t <= T; ++t)
-          stage2d<true, VAR, NL, V, S, BAND>(p, w[t][ph % 3], w[t][(ph + 1) % 3],
+          stage2d<true, VAR, NL, RECIP, V, S, BAND>(p, w[t][ph % 3], w[t][(ph + 1) % 3],
                                              w[t][(ph + 2) % 3], x, ring_f, slot - t, lane,
-                                             rho - t, p.omega[t - 1], use_recip, lane_col, i0,
+                                             rho - t, p.omega[t - 1], lane_col, i0,
                                              i1, own_c0, own_c1, f_lo, f_hi, rmx[t - 1],
                                              dmx[t - 1]);
       } else {
 #pragma unroll
         for (int t = 1; t <= T; ++t)
-          stage2d<false, VAR, NL, V, S, BAND>(p, w[t][ph % 3], w[t][(ph + 1) % 3],
+          stage2d<false, VAR, NL, RECIP, V, S, BAND>(p, w[t][ph % 3], w[t][(ph + 1) % 3],
                                               w[t][(ph + 2) % 3], x, ring_f, slot - t, lane,
-                                              rho - t, p.omega[t - 1], use_recip, lane_col, i0,
+                                              rho - t, p.omega[t - 1], lane_col, i0,
                                               i1, own_c0, own_c1, f_lo, f_hi, rmx[t - 1],
                                               dmx[t - 1]);
       }
@@ -293,7 +328,7 @@ __global__ void __launch_bounds__(Band2D<T>::WARPS * 32)
       dm = warp_max(fabs(dmx[t]));
     } else {
       const double num = __dmul_rn(p.omega[t], rm);
-      dm = fabs(use_recip ? div_by_const(num, p.kc, p.kinv) : __ddiv_rn(num, p.kc));
+      dm = fabs(__ddiv_rn(num, p.kc));
     }
     if (lane == 0) {
       global_max(p.norms + 2 * t, dm);
