@@ -4,6 +4,8 @@
 // :602-687): the caller (Python, ctypes) owns all device buffers; this layer
 // plans the launch geometry, picks the fused-sweep depth, launches the
 // kernels on the caller's stream and reports errors as status codes.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -75,37 +77,41 @@ int sm_count() {
 // (registers and shared memory both counted, from the occupancy API), so the
 // launch can be sized to exactly one wave.
 struct Kernel2D {
-  void (*launch)(const Sweep2DParams &, int blocks, cudaStream_t);
+  void (*launch)(const Sweep2DParams &, const CUtensorMap &, const CUtensorMap &, int blocks,
+                 cudaStream_t);
+  int box_cols;
   int (*blocks_per_sm)();
   int own;  // columns owned per band
 };
 
 template <int T, bool VAR, bool NL, bool RECIP>
 struct K2 {
-  using B = Band2D<T>;
+  static constexpr int V = 2;
+  using B = Band2D<T, V>;
   static void configure() {
     static bool done = false;
     if (!done) {
-      cudaFuncSetAttribute(sweep2d_tb<T, VAR, NL, RECIP>,
+      cudaFuncSetAttribute(sweep2d_tb<T, V, VAR, NL, RECIP>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(B::smem_bytes()));
       done = true;
     }
   }
-  static void launch(const Sweep2DParams &p, int blocks, cudaStream_t s) {
+  static void launch(const Sweep2DParams &p, const CUtensorMap &tu, const CUtensorMap &tf,
+                     int blocks, cudaStream_t s) {
     configure();
-    sweep2d_tb<T, VAR, NL, RECIP><<<blocks, B::WARPS * 32, B::smem_bytes(), s>>>(p);
+    sweep2d_tb<T, V, VAR, NL, RECIP><<<blocks, B::WARPS * 32, B::smem_bytes(), s>>>(p, tu, tf);
   }
   static int bps() {
     static int n = 0;
     if (n == 0) {
       configure();
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_tb<T, VAR, NL, RECIP>,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_tb<T, V, VAR, NL, RECIP>,
                                                     B::WARPS * 32, B::smem_bytes());
       if (n <= 0) n = 1;
     }
     return n;
   }
-  static Kernel2D get() { return Kernel2D{launch, bps, B::OWN}; }
+  static Kernel2D get() { return Kernel2D{launch, B::BAND, bps, B::OWN}; }
 };
 
 template <int T>
@@ -113,6 +119,36 @@ Kernel2D pick2d_t(bool var, bool nl, bool recip) {
   if (var) return nl ? K2<T, true, true, false>::get() : K2<T, true, false, false>::get();
   if (recip) return nl ? K2<T, false, true, true>::get() : K2<T, false, false, true>::get();
   return nl ? K2<T, false, true, false>::get() : K2<T, false, false, false>::get();
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 2D tensor map over a whole padded 2D field: rows0 rows of `pitch` doubles,
+// box = box_cols x 3 rows (one TMA group of the band kernel).
+int make_tmap(CUtensorMap *m, const double *base, const srj_layout_t &l, int box_cols) {
+  auto fn = encode_fn();
+  if (!fn) return fail(SRJ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cuuint64_t(l.pitch), cuuint64_t(l.rows0)};
+  cuuint64_t strides[1] = {cuuint64_t(l.pitch) * 8};
+  cuuint32_t box[2] = {cuuint32_t(box_cols), 3};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SRJ_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return SRJ_OK;
 }
 
 Kernel2D pick2d(int T, bool var, bool nl, bool recip) {
@@ -348,16 +384,23 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       const Kernel2D k2 = pick2d(t, var, nl, !var && p.kinv != 0.0);
       p.nbands = int((l.n[1] + k2.own - 1) / k2.own);
       // exactly one wave: strips x bands <= resident warps
-      const int capacity = sm_count() * k2.blocks_per_sm() * Band2D<1>::WARPS;
+      const int capacity = sm_count() * k2.blocks_per_sm() * Band2D<1, 2>::WARPS;
       int nstrips = std::max(1, capacity / p.nbands);
       nstrips = std::min(nstrips, std::max(1, rows / std::max(2 * t, 8)));
       p.H = (rows + nstrips - 1) / nstrips;
       p.nstrips = (rows + p.H - 1) / p.H;
       for (int q = 0; q < t; ++q) p.omega[q] = weights[(first + k + q) % m];
       p.norms = d_norms + 2 * k;
+      p.tma_col0 = int(l.origin + 1);
+      p.tma_row0 = l.halo0;
+      CUtensorMap tu, tf;
+      int rc = make_tmap(&tu, cur, l, k2.box_cols);
+      if (rc != SRJ_OK) return rc;
+      rc = make_tmap(&tf, f, l, k2.box_cols);
+      if (rc != SRJ_OK) return rc;
       const int warps = p.nbands * p.nstrips;
-      const int blocks = (warps + Band2D<1>::WARPS - 1) / Band2D<1>::WARPS;
-      k2.launch(p, blocks, st);
+      const int blocks = (warps + Band2D<1, 2>::WARPS - 1) / Band2D<1, 2>::WARPS;
+      k2.launch(p, tu, tf, blocks, st);
     } else {
       Sweep3DParams p{};
       p.src = cur + ioff;

@@ -2,19 +2,24 @@
 //
 // One warp streams a column band of the grid down axis 0 and applies T
 // consecutive SRJ steps (each with its own omega_k) in a single pass over HBM:
-// stage t (t = 1..T) turns stage t-1 rows into step k+t rows, with a one-row
-// lag per stage, entirely in registers.  Horizontal neighbours move with warp
+// stage t (t = 1..T) turns stage t-1 rows into step k+t rows entirely in
+// registers.  The pipeline is skewed by two rows per stage -- at tick tau stage
+// t relaxes row tau-2t from stage t-1 rows produced in EARLIER ticks -- so the
+// T stages of a tick carry no dependency on each other and their DP chains
+// overlap (instruction-level parallelism T x V per lane).  Horizontal neighbours move with warp
 // shuffles; bands overlap by TP >= T columns per side so every owned column is
 // exact at stage T (the overlap cells are recomputed, never stored).
 //
-// Stage-0 rows (u^k) and the source rows arrive through a per-warp ring of S
-// shared-memory slots filled by the TMA engine (cp.async.bulk, completion on
-// one mbarrier per slot).  The slot of tick tau is recycled after stage T
-// consumed its source row at tick tau+T, so loads run S-T-1 rows ahead.
+// Rows arrive in groups of G = 3 (the window period): one 2D TMA tensor copy
+// (cp.async.bulk.tensor.2d, box BAND x 3) for u^k and one for the source per
+// group, completing on one mbarrier per ring slot.  A slot is recycled once
+// the last stage has read its source rows (ceil(2T/3) groups later), so loads
+// run NS - ceil(2T/3) - 1 groups ahead.
 //
 // Instruction economy (the kernel is issue-bound, not HBM-bound, at T>=2):
 //  * the row window of each stage rotates by register renaming -- the tick
 //    loop is unrolled by 3, the window period;
+//  * one warp vote per tick for the rare IEEE-division fixups;
 //  * interior ticks of interior bands take a predicate-free path;
 //  * with a constant stencil only max|r| is tracked per step: |d| =
 //    |RN(RN(omega*r)/c)| is a monotone function of |r|, so
@@ -28,6 +33,8 @@
 // _wj2 (grids.py:351-376); ghost rows/columns and inactive (masked) cells pass
 // their value through unchanged (grids.py:374-375, FIXED ghosts :225-247).
 #pragma once
+#include <cuda.h>
+
 #include "srj_device.cuh"
 
 namespace srj {
@@ -46,24 +53,27 @@ struct Sweep2DParams {
   int ld_lo, ld_hi;    // rows present in memory: [ld_lo, ld_hi]
   int own_b, own_e;    // rows stored + counted in the norms
   int H, nbands, nstrips;
+  int tma_col0;        // tensor-map column of interior column 0
+  int tma_row0;        // tensor-map row of interior row 0
   double omega[kMaxFuse];
   double *norms;       // [T][2]: (dmax, rmax) per fused step
 };
 
-template <int T>
+template <int T, int V_ = 2>
 struct Band2D {
-  static constexpr int V = 4;                    // columns per lane
+  static constexpr int V = V_;                   // columns per lane
   static constexpr int BAND = 32 * V;            // columns per warp
   static constexpr int TP = (T + V - 1) / V * V; // overlap: whole lanes
   static constexpr int OWN = BAND - 2 * TP;      // columns a band owns
-  static constexpr int S = (T + 4 <= 8) ? 8 : 16;  // ring slots (power of 2)
-  static constexpr int LOG_S = (S == 8) ? 3 : 4;
-  static constexpr int WARPS = 4;
-  static constexpr int ROW_BYTES = BAND * 8;
-  static constexpr int SLOT_BYTES = 2 * ROW_BYTES;  // u row + source row
-  static constexpr size_t smem_bytes() {
-    return size_t(WARPS) * S * SLOT_BYTES + size_t(WARPS) * S * 8;
-  }
+  static constexpr int G = 3;                    // rows per TMA group
+  static constexpr int LAG = (2 * T + G - 1) / G;  // groups a source row stays live
+  static constexpr int NS = (LAG + 5 <= 8) ? 8 : 16;  // ring slots (power of 2)
+  static constexpr int LOG_NS = (NS == 8) ? 3 : 4;
+  static constexpr int WARPS = 2;
+  static constexpr int BOX_BYTES = G * BAND * 8;      // one array, one group
+  static constexpr int SLOT_BYTES = 2 * BOX_BYTES;    // u box + source box
+  static constexpr int WARP_BYTES = (NS * SLOT_BYTES + NS * 8 + 127) / 128 * 128;
+  static constexpr size_t smem_bytes() { return size_t(WARPS) * WARP_BYTES + 128; }
 };
 
 // RN(a/c) for a fixed divisor c > 0 with y = RN(1/c), branch-free:
@@ -101,19 +111,17 @@ __device__ __forceinline__ void acc_absmax(double &m, double x) {
   m = (fabs(x) > fabs(m)) ? x : m;
 }
 
-// One stage of the fused pipeline for the lane's V cells: the window rows
-// (up, mid) hold stage t-1 rows r-1, r; x arrives holding row r+1 and leaves
-// holding the stage-t value of row r.
-template <bool FAST, bool VAR, bool NL, bool RECIP, int V, int S, int BAND>
-__device__ __forceinline__ void stage2d(const Sweep2DParams &p, double (&up)[V], double (&mid)[V],
-                                        double (&down)[V], double (&x)[V],
-                                        const double *ring_f, int fslot, int lane, int r,
-                                        double om, int lane_col, int i0, int i1,
-                                        int own_c0, int own_c1, int f_lo, int f_hi, double &rmx,
-                                        double &dmx) {
-#pragma unroll
-  for (int v = 0; v < V; ++v) down[v] = x[v];
-  const double *frow = ring_f + (fslot & (S - 1)) * BAND + V * lane;
+// One stage of the skewed pipeline for the lane's V cells.  (up, mid, down)
+// hold stage t-1 rows r-1, r, r+1, all produced in earlier ticks, so the T
+// stages of a tick are mutually independent.  Writes the stage-t value of row
+// r to y and the numerators to num; bad collects div_recip range failures.
+template <bool FAST, bool EDGE, bool VAR, bool NL, bool RECIP, int V>
+__device__ __forceinline__ void stage2d(const Sweep2DParams &p, const double (&up)[V],
+                                        const double (&mid)[V], const double (&down)[V],
+                                        const double *frow, int r, double om, int lane_col,
+                                        int i0, int i1, int own_c0, int own_c1, int f_lo,
+                                        int f_hi, unsigned colact, double (&y)[V],
+                                        double (&num)[V], double &rmx, double &dmx, bool &bad) {
   double fv[V];
 #pragma unroll
   for (int v = 0; v < V; v += 2) {
@@ -130,7 +138,7 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, double (&up)[V],
     row_own = (r >= i0) && (r < i1);
     rc = min(max(r, f_lo), f_hi);
   }
-  double num[V], cv[V];
+  double cv[V];
   bool actv[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -152,60 +160,85 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, double (&up)[V],
         if (p.act) act = act && (__ldg(p.act + q) != 0);
       }
     }
+    if (FAST && EDGE) act = (colact >> v) & 1u;
     const double s = NL ? nl_source(fv[v], uc) : fv[v];
     const double rr = resid5(s, c, uc, a0, up[v], b0, down[v], a1, uw, b1, ue);
-    num[v] = __dmul_rn(om, rr);
-    if (!FAST && !act) num[v] = 0.0;  // passthrough cell: keep garbage off the slow path
+    double nm = __dmul_rn(om, rr);
+    if ((!FAST || EDGE) && !act) nm = 1.0;  // passthrough cell: keep garbage off the slow path
+    num[v] = nm;
     cv[v] = c;
     actv[v] = act;
-    if (FAST) {
+    if (FAST && !EDGE) {
+      acc_absmax(rmx, rr);  // garbage lanes are excluded at the warp vote
+    } else if (FAST) {
+      if ((colact >> (V + v)) & 1u) acc_absmax(rmx, rr);  // owned-column bit
+    } else if (act && row_own && col >= own_c0 && col < own_c1) {
       acc_absmax(rmx, rr);
-    } else if (act && (r >= i0) && (r < i1) && col >= own_c0 && col < own_c1) {
-      acc_absmax(rmx, rr);
     }
-  }
-  double d[V];
-  if (RECIP) {
-    bool bad = false;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      d[v] = div_recip(num[v], p.kc, p.kinv);
-      bad |= recip_unsafe(num[v]);
-    }
-    if (__any_sync(kFull, bad)) {
-#pragma unroll
-      for (int v = 0; v < V; ++v)
-        if (recip_unsafe(num[v])) d[v] = div_ieee(num[v], p.kc);
-    }
-  } else {
-#pragma unroll
-    for (int v = 0; v < V; ++v) d[v] = __ddiv_rn(num[v], cv[v]);
   }
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const double uc = mid[v];
-    if (FAST) {
-      x[v] = __dadd_rn(uc, d[v]);
+    double d;
+    if (RECIP) {
+      d = div_recip(num[v], p.kc, p.kinv);
+      bad |= recip_unsafe(num[v]);
     } else {
-      x[v] = actv[v] ? __dadd_rn(uc, d[v]) : uc;
-      if (VAR && actv[v] && row_own && lane_col + v >= own_c0 && lane_col + v < own_c1)
-        acc_absmax(dmx, d[v]);
+      d = __ddiv_rn(num[v], cv[v]);
+    }
+    if (FAST && !EDGE) {
+      y[v] = __dadd_rn(uc, d);
+    } else {
+      y[v] = actv[v] ? __dadd_rn(uc, d) : uc;
+      if (!FAST && VAR && actv[v] && row_own && lane_col + v >= own_c0 && lane_col + v < own_c1)
+        acc_absmax(dmx, d);
     }
   }
 }
 
-template <int T, bool VAR, bool NL, bool RECIP>
-__global__ void __launch_bounds__(Band2D<T>::WARPS * 32)
-    sweep2d_tb(const __grid_constant__ Sweep2DParams p) {
-  using B = Band2D<T>;
-  constexpr int V = B::V, BAND = B::BAND, TP = B::TP, OWN = B::OWN, S = B::S;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+// Redo the cells whose numerator fell outside div_recip's range with the IEEE
+// division (rare: zero/subnormal/huge/inf/NaN numerators).
+template <bool FAST, bool EDGE, int V>
+__device__ __forceinline__ void fix_stage(const Sweep2DParams &p, const double (&mid)[V],
+                                          const double (&num)[V], int r, int lane_col,
+                                          unsigned colact, double (&y)[V]) {
+  const bool row_act = FAST || ((r >= p.lo_c) && (r < p.hi_c));
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int col = lane_col + v;
+    bool act = FAST || (row_act && col >= 0 && col < p.n1);
+    if (FAST && EDGE) act = (colact >> v) & 1u;
+    if (act && recip_unsafe(num[v])) y[v] = __dadd_rn(mid[v], div_ieee(num[v], p.kc));
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+template <int T, int V, bool VAR, bool NL, bool RECIP>
+__global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
+    sweep2d_tb(const __grid_constant__ Sweep2DParams p, const __grid_constant__ CUtensorMap tm_u,
+               const __grid_constant__ CUtensorMap tm_f) {
+  using B = Band2D<T, V>;
+  constexpr int BAND = B::BAND, TP = B::TP, OWN = B::OWN, NS = B::NS, G = B::G, LAG = B::LAG;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  double *ring_u = reinterpret_cast<double *>(smem_raw) + size_t(warp) * S * 2 * BAND;
-  double *ring_f = ring_u + S * BAND;
-  uint64_t *bars =
-      reinterpret_cast<uint64_t *>(smem_raw + size_t(B::WARPS) * S * B::SLOT_BYTES) + warp * S;
+  unsigned char *wbase = smem + size_t(warp) * B::WARP_BYTES;
+  double *ring = reinterpret_cast<double *>(wbase);  // slot s: u box, then source box
+  uint64_t *bars = reinterpret_cast<uint64_t *>(wbase + NS * B::SLOT_BYTES);
 
   const int gw = blockIdx.x * B::WARPS + warp;
   const int band = gw % p.nbands;
@@ -215,43 +248,52 @@ __global__ void __launch_bounds__(Band2D<T>::WARPS * 32)
   const int i0 = p.own_b + strip * p.H;
   const int i1 = min(i0 + p.H, p.own_e);
   const int rho_b = max(i0 - T, p.ld_lo);
-  const int nreal = i1 + T - rho_b;            // last real tick emits stage-T row i1-1
-  const int nticks = (nreal + 2) / 3 * 3;      // extra ticks emit unowned rows only
+  const int nreal = i1 + 2 * T - rho_b;        // last real tick emits stage-T row i1-1
+  const int ngroups = (nreal + G - 1) / G;     // extra ticks emit unowned rows only
   const int col_band = band * OWN - TP;
   const int own_c0 = band * OWN;
   const int own_c1 = min(own_c0 + OWN, p.n1);
   const int f_lo = p.lo_c, f_hi = p.hi_c - 1;
   const bool band_interior = (col_band >= 0) && (col_band + BAND <= p.n1) && !VAR;
-  // fast ticks: all T stage rows owned and relaxing
-  const int fast_lo = max(i0, p.lo_c) + T;     // rho >= fast_lo  <=> rho - T >= ...
-  const int fast_hi = min(i1, p.hi_c);         // rho - 1 < fast_hi
+  const bool band_edge = !band_interior && !VAR;  // fast rows, masked columns
+  // fast ticks: every stage row rho-2t (t=1..T) owned and relaxing
+  const int fast_lo = max(i0, p.lo_c) + 2 * T;
+  const int fast_hi = min(i1, p.hi_c) + 1;
   const int lane_col = col_band + V * lane;
   const bool lane_owned = (lane_col >= own_c0) && (lane_col + V <= own_c1);
+  // bit v: column lane_col+v is interior (relaxes); bit V+v: it is owned
+  unsigned colact = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    if (lane_col + v >= 0 && lane_col + v < p.n1) colact |= 1u << v;
+    if (lane_col + v >= own_c0 && lane_col + v < own_c1) colact |= 1u << (V + v);
+  }
+  const int tma_col = p.tma_col0 + col_band;
+  const int tma_row = p.tma_row0 + rho_b;
 
-  auto issue = [&](int slot, int tick) {
-    const int r = rho_b + tick;
-    const int ru = min(max(r, p.ld_lo), p.ld_hi);
-    const int rf = min(max(r, f_lo), f_hi);
-    mbar_expect_tx(&bars[slot], B::SLOT_BYTES);
-    bulk_g2s(ring_u + slot * BAND, p.src + int64_t(ru) * p.pitch + col_band, B::ROW_BYTES,
-             &bars[slot]);
-    bulk_g2s(ring_f + slot * BAND, p.f + int64_t(rf) * p.pitch + col_band, B::ROW_BYTES,
-             &bars[slot]);
+  auto issue = [&](int g) {
+    const int s = g & (NS - 1);
+    double *slot = ring + s * (B::SLOT_BYTES / 8);
+    mbar_expect_tx(&bars[s], B::SLOT_BYTES);
+    tma_load_2d(slot, &tm_u, tma_col, tma_row + G * g, &bars[s]);
+    tma_load_2d(slot + G * BAND, &tm_f, tma_col, tma_row + G * g, &bars[s]);
   };
 
   if (lane == 0) {
+    tma_prefetch_desc(&tm_u);
+    tma_prefetch_desc(&tm_f);
 #pragma unroll 1
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
 #pragma unroll 1
-    for (int s = 0; s < S && s < nticks; ++s) issue(s, s);
+    for (int g = 0; g < NS && g < ngroups; ++g) issue(g);
   }
   __syncwarp();
 
-  double w[T + 1][3][V];  // w[t]: 3-row window of stage t's input (stage t-1 rows)
+  double w[T + 2][3][V];  // w[t]: window of stage t (rows of stage t-1); w[T+1] unused
   double rmx[T], dmx[T];
 #pragma unroll
-  for (int t = 0; t <= T; ++t)
+  for (int t = 0; t <= T + 1; ++t)
 #pragma unroll
     for (int k = 0; k < 3; ++k)
 #pragma unroll
@@ -259,76 +301,92 @@ __global__ void __launch_bounds__(Band2D<T>::WARPS * 32)
 #pragma unroll
   for (int t = 0; t < T; ++t) rmx[t] = dmx[t] = 0.0;
 
+  double *out = p.dst + int64_t(rho_b - 2 * T) * p.pitch + lane_col;  // row of tick 0's output
+
 #pragma unroll 1
-  for (int it0 = 0; it0 < nticks; it0 += 3) {
+  for (int g = 0; g < ngroups; ++g) {
+    const int s = g & (NS - 1);
+    mbar_wait(&bars[s], (g >> B::LOG_NS) & 1);
 #pragma unroll
-    for (int ph = 0; ph < 3; ++ph) {
-      const int it = it0 + ph;
+    for (int ph = 0; ph < G; ++ph) {
+      const int it = G * g + ph;
       const int rho = rho_b + it;
-      const int slot = it & (S - 1);
-      mbar_wait(&bars[slot], (it >> B::LOG_S) & 1);
-      double x[V];
-      {
-        const double *urow = ring_u + slot * BAND + V * lane;
+      double num[T + 1][V], yT[V];
+      bool bad = false;
+      const bool fast_rows = rho >= fast_lo && rho <= fast_hi;
+      // stages in descending order: stage t reads its window, then stage t-1
+      // writes its output into stage t's free window row (no register copies)
+#define SRJ_STAGE(FASTV, EDGEV)                                                                      \
+  _Pragma("unroll") for (int t = T; t >= 1; --t) {                                            \
+    const int fg = g + ((ph - 2 * t) >= 0 ? 0 : -((2 * t - ph + G - 1) / G));                 \
+    const int fr = ph - 2 * t + G * (g - fg);                                                 \
+    const double *frow = ring + (fg & (NS - 1)) * (B::SLOT_BYTES / 8) + G * BAND + fr * BAND + \
+                         V * lane;                                                            \
+    double(&dst)[V] = (t == T) ? yT : w[t + 1][ph % 3];                                       \
+    stage2d<FASTV, EDGEV, VAR, NL, RECIP, V>(p, w[t][ph % 3], w[t][(ph + 1) % 3],            \
+                                      w[t][(ph + 2) % 3], frow, rho - 2 * t, p.omega[t - 1],  \
+                                      lane_col, i0, i1, own_c0, own_c1, f_lo, f_hi, colact,   \
+                                      dst, num[t], rmx[t - 1], dmx[t - 1], bad);              \
+  }                                                                                           \
+  if (RECIP && __any_sync(kFull, bad)) {                                                      \
+    _Pragma("unroll") for (int t = T; t >= 1; --t) {                                          \
+      double(&dst)[V] = (t == T) ? yT : w[t + 1][ph % 3];                                     \
+      fix_stage<FASTV, EDGEV, V>(p, w[t][(ph + 1) % 3], num[t], rho - 2 * t, lane_col, colact, \
+                                 dst);                                                        \
+    }                                                                                         \
+  }
+      if (band_interior && fast_rows) {
+        SRJ_STAGE(true, false)
+      } else if (band_edge && fast_rows) {
+        SRJ_STAGE(true, true)
+      } else {
+        SRJ_STAGE(false, false)
+      }
+#undef SRJ_STAGE
+      {  // stage 0: the freshly loaded row enters stage 1's window
+        const double *urow = ring + s * (B::SLOT_BYTES / 8) + ph * BAND + V * lane;
 #pragma unroll
         for (int v = 0; v < V; v += 2) {
           const double2 q = *reinterpret_cast<const double2 *>(urow + v);
-          x[v] = q.x;
-          x[v + 1] = q.y;
+          w[1][ph % 3][v] = q.x;
+          w[1][ph % 3][v + 1] = q.y;
         }
       }
-      if (band_interior && rho >= fast_lo && rho <= fast_hi) {
-#pragma unroll
-        for (int t = 1; t <= T; ++t)
-          stage2d<true, VAR, NL, RECIP, V, S, BAND>(p, w[t][ph % 3], w[t][(ph + 1) % 3],
-                                             w[t][(ph + 2) % 3], x, ring_f, slot - t, lane,
-                                             rho - t, p.omega[t - 1], lane_col, i0,
-                                             i1, own_c0, own_c1, f_lo, f_hi, rmx[t - 1],
-                                             dmx[t - 1]);
-      } else {
-#pragma unroll
-        for (int t = 1; t <= T; ++t)
-          stage2d<false, VAR, NL, RECIP, V, S, BAND>(p, w[t][ph % 3], w[t][(ph + 1) % 3],
-                                              w[t][(ph + 2) % 3], x, ring_f, slot - t, lane,
-                                              rho - t, p.omega[t - 1], lane_col, i0,
-                                              i1, own_c0, own_c1, f_lo, f_hi, rmx[t - 1],
-                                              dmx[t - 1]);
-      }
-      const int rs = rho - T;  // x holds stage-T row rs
+      const int rs = rho - 2 * T;  // yT holds stage-T row rs
       if (rs >= i0 && rs < i1) {
-        double *o = p.dst + int64_t(rs) * p.pitch + lane_col;
         if (lane_owned) {
 #pragma unroll
           for (int v = 0; v < V; v += 2)
-            *reinterpret_cast<double2 *>(o + v) = make_double2(x[v], x[v + 1]);
+            *reinterpret_cast<double2 *>(out + v) = make_double2(yT[v], yT[v + 1]);
         } else {
 #pragma unroll
           for (int v = 0; v < V; ++v) {
             const int col = lane_col + v;
-            if (col >= own_c0 && col < own_c1) o[v] = x[v];
+            if (col >= own_c0 && col < own_c1) out[v] = yT[v];
           }
         }
       }
-      __syncwarp();
-      if (lane == 0 && it >= T && it - T + S < nticks) {
-        fence_proxy_async();
-        issue((it - T) & (S - 1), it - T + S);
-      }
+      out += p.pitch;
+    }
+    __syncwarp();
+    if (lane == 0 && g >= LAG && g - LAG + NS < ngroups) {
+      fence_proxy_async();
+      issue(g - LAG + NS);
     }
   }
 
-  // per-step norms: lanes outside the owned columns may hold garbage from
-  // fast ticks; they do not vote
+  // per-step norms: in interior bands the fast ticks accumulate every lane
+  // (non-owned lanes hold garbage) so only owned lanes vote; edge bands and
+  // predicated ticks accumulate owned cells only
 #pragma unroll
   for (int t = 0; t < T; ++t) {
-    const double rl = lane_owned || !band_interior ? fabs(rmx[t]) : 0.0;
+    const double rl = (!band_interior || lane_owned) ? fabs(rmx[t]) : 0.0;
     const double rm = warp_max(rl);
     double dm;
-    if constexpr (VAR) {
+    if (VAR) {
       dm = warp_max(fabs(dmx[t]));
     } else {
-      const double num = __dmul_rn(p.omega[t], rm);
-      dm = fabs(__ddiv_rn(num, p.kc));
+      dm = fabs(__ddiv_rn(__dmul_rn(p.omega[t], rm), p.kc));
     }
     if (lane == 0) {
       global_max(p.norms + 2 * t, dm);
