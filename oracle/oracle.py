@@ -167,8 +167,12 @@ def residual(problem, kappa=None):
     return float(out[0]), float(out[1])
 
 
-def np_step(problem, omega, kappa=None):
-    """numpy restatement of ``_jacobi_step_numpy`` (grids.py:491-504)."""
+def np_step(problem, omega, kappa=None, own_rows=None):
+    """numpy restatement of ``_jacobi_step_numpy`` (grids.py:491-504).
+
+    ``own_rows=(lo, hi)`` restricts the returned norms to interior rows
+    [lo, hi) of axis 0 (slab-decomposition checks); the update is unchanged.
+    """
     nd = problem.center.ndim
     core = (slice(1, -1),) * nd
     u = problem.u
@@ -192,8 +196,13 @@ def np_step(problem, omega, kappa=None):
     if act is None:
         act = np.ones(problem.center.shape, dtype=bool)
     new = np.where(act, uc + d, uc)
-    dmax = float(np.max(np.abs(d[act]), initial=0.0))
-    rmax = float(np.max(np.abs(r[act]), initial=0.0))
+    sel = np.broadcast_to(act, d.shape).copy()
+    if own_rows is not None:
+        keep = np.zeros(d.shape[0], dtype=bool)
+        keep[own_rows[0]:own_rows[1]] = True
+        sel &= keep.reshape((-1,) + (1,) * (d.ndim - 1))
+    dmax = float(np.max(np.abs(d[sel]), initial=0.0))
+    rmax = float(np.max(np.abs(r[sel]), initial=0.0))
     u[core] = new
     return dmax, rmax
 

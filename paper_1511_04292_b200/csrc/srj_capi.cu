@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/srj.h"
@@ -59,6 +60,17 @@ double recip_or_zero(double c) {
 // offset of interior cell (0,0[,0])
 int64_t interior_offset(const srj_layout_t &l) {
   return l.origin + int64_t(l.halo0) * l.plane + (l.ndim == 3 ? l.pitch : 0) + 1;
+}
+
+// SRJ_WAVES=<n>: launch n waves of band warps instead of one (tuning knob)
+int waves_2d() {
+  static int w = 0;
+  if (w == 0) {
+    const char *e = getenv("SRJ_WAVES");
+    w = e ? atoi(e) : 1;
+    if (w < 1 || w > 64) w = 1;
+  }
+  return w;
 }
 
 int sm_count() {
@@ -383,8 +395,8 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.own_e = int(d.own0_end);
       const Kernel2D k2 = pick2d(t, var, nl, !var && p.kinv != 0.0);
       p.nbands = int((l.n[1] + k2.own - 1) / k2.own);
-      // exactly one wave: strips x bands <= resident warps
-      const int capacity = sm_count() * k2.blocks_per_sm() * Band2D<1, 2>::WARPS;
+      // strips x bands = waves x resident warps (default one wave)
+      const int capacity = sm_count() * k2.blocks_per_sm() * Band2D<1, 2>::WARPS * waves_2d();
       int nstrips = std::max(1, capacity / p.nbands);
       nstrips = std::min(nstrips, std::max(1, rows / std::max(2 * t, 8)));
       p.H = (rows + nstrips - 1) / nstrips;

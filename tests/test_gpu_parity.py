@@ -276,3 +276,64 @@ def test_reciprocal_division_is_correctly_rounded(c):
         torch.cuda.synchronize()
         same = (out.view(torch.int64) == ref.view(torch.int64)) | (torch.isnan(out) & torch.isnan(ref))
         assert bool(same.all()), f"{int((~same).sum())} mismatches for c={c}"
+
+
+# ------------------------------------------------- slab decomposition on 1 GPU
+class _EmulatedRanks:
+    """k DeviceSlab backends in one process, exchanging halos by device copies
+    (no kernels wait on each other; the NCCL path is covered by the gloo tests
+    in test_distributed.py with the same SlabDecomposition plan)."""
+
+    def __init__(self, fields, world, fuse):
+        from paper_1511_04292_b200.distributed import DeviceSlab, SlabDecomposition
+
+        n0 = fields["source"].shape[0]
+        self.d = [SlabDecomposition(n0, world, r, halo=fuse) for r in range(world)]
+        self.b = [DeviceSlab(fields, d) for d in self.d]
+        self.fuse = fuse
+
+    def run(self, w, nsteps):
+        import torch
+
+        for b in self.b:
+            b.reserve(nsteps)
+        cur, k, flip = 0, 0, 0
+        others = [1, 2]
+        while k < nsteps:
+            t = min(self.fuse, nsteps - k)
+            dst = others[flip]
+            for b in self.b:
+                b.run(cur, dst, w, k, t, k)
+            for r, d in enumerate(self.d):  # rank r receives from its neighbours
+                for peer, first, count in d.recvs():
+                    src_first = [s for s in self.d[peer].sends() if s[0] == r][0][1]
+                    self.b[r].layers(dst, first, count).copy_(
+                        self.b[peer].layers(dst, src_first, count))
+            cur, flip, k = dst, 1 - flip, k + t
+        torch.cuda.synchronize()
+        norms = np.max([b.norms(nsteps).cpu().numpy() for b in self.b], axis=0)
+        field = np.concatenate([b.download_owned(cur) for b in self.b])
+        return field, norms.reshape(nsteps, 2)
+
+
+@pytest.mark.parametrize("world,fuse", [(2, 4), (4, 3), (3, 1)])
+def test_slab_decomposition_bitwise_on_one_gpu(table, world, fuse):
+    """k-rank slab solve == single-GPU solve bit for bit (cfg2 recipe)."""
+    f = config_fields("cfg2", (331, 270))
+    w = quantize(table.lookup(6, 4096)).weight_sequence
+    ranks = _EmulatedRanks(f, world, fuse)
+    field, norms = ranks.run(w, 97)
+    p = problem_from(f)
+    hist, _ = run_steps(p, w, 97, fuse=fuse)
+    assert np.array_equal(field, p.interior)
+    assert np.array_equal(norms[:, 1], hist.true_residual_inf)
+
+
+def test_slab_decomposition_3d_on_one_gpu(table):
+    f = config_fields("cfg3", (37, 30, 66))
+    w = quantize(table.lookup(10, 512)).weight_sequence
+    field, norms = _EmulatedRanks(f, 3, 1).run(w, 40)
+    p = problem_from(f)
+    hist, _ = run_steps(p, w, 40)
+    assert np.array_equal(field, p.interior)
+    assert np.array_equal(norms[:, 1], hist.true_residual_inf)
