@@ -97,6 +97,15 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def ncu_traffic(fuse, cells):
+    """DRAM bytes per launch from the committed ncu capture of this kernel."""
+    path = os.path.join(ROOT, "profiles", f"round1_ncu_sweep2d_T{fuse}.json")
+    if not os.path.exists(path) or cells != 4096 * 4096:
+        return None
+    with open(path) as fh:
+        return json.load(fh).get("dram_traffic_bytes_per_launch")
+
+
 def schedule():
     from paper_1511_04292_b200.schedule import quantize
     from paper_1511_04292_b200.tables import shipped_table
@@ -264,6 +273,7 @@ def run_gpu(args):
     avg_launch_ms = kernel_ms / (args.steps * launches_per_cycle)
     peak, peak_kind = peaks()
     achieved = cells_rank * T * BYTES_PER_UPDATE / (avg_launch_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(T, cells_rank)
 
     e2e = None
     cpu = None
@@ -287,7 +297,11 @@ def run_gpu(args):
                    "fuse": T, "l2": "inputs larger than L2 (3 x 134 MB streamed per sweep)",
                    "parallelism": f"row-block x{ws}" if ws > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                     "of the same kernel/size (profiles/round1_ncu_sweep2d_T4.json); "
+                                     "actual HBM bytes vs algorithmic shows the temporal-blocking "
+                                     "saving",
                      "peak_kind": peak_kind,
                      "kernel": f"sweep2d_tb<T={T}> (fused {T} sweeps/launch)",
                      "algorithmic_bytes_per_launch": cells_rank * T * BYTES_PER_UPDATE,
