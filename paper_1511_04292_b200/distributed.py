@@ -225,7 +225,8 @@ class DeviceSlab:
         u = np.empty(tuple(int(x) + 2 for x in self.grid.shape))
         self.grid.download_field(buf, u)
         lo, hi = self.grid.desc.own0_begin, self.grid.desc.own0_end
-        return u[1 + lo:1 + hi]
+        inner = (slice(1, -1),) * (u.ndim - 1)
+        return u[(slice(1 + lo, 1 + hi),) + inner]
 
 
 class SlabGrid:
