@@ -133,6 +133,34 @@ Kernel2D pick2d_t(bool var, bool nl, bool recip) {
   return nl ? K2<T, false, true, false>::get() : K2<T, false, false, false>::get();
 }
 
+// ------------------------------------------------------------ 3D dispatch
+struct Kernel3D {
+  void (*launch)(const Sweep3DParams &, int blocks, cudaStream_t);
+  int (*blocks_per_sm)();
+};
+
+template <bool VAR, bool NL, bool RECIP>
+struct K3 {
+  static void launch(const Sweep3DParams &p, int blocks, cudaStream_t s) {
+    sweep3d<VAR, NL, RECIP><<<blocks, kWarps3D * 32, 0, s>>>(p);
+  }
+  static int bps() {
+    static int n = 0;
+    if (n == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d<VAR, NL, RECIP>, kWarps3D * 32, 0);
+      if (n <= 0) n = 1;
+    }
+    return n;
+  }
+  static Kernel3D get() { return Kernel3D{launch, bps}; }
+};
+
+Kernel3D pick3d(bool var, bool nl, bool recip) {
+  if (var) return nl ? K3<true, true, false>::get() : K3<true, false, false>::get();
+  if (recip) return nl ? K3<false, true, true>::get() : K3<false, false, true>::get();
+  return nl ? K3<false, true, false>::get() : K3<false, false, false>::get();
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -436,22 +464,31 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.own_b = int(d.own0_begin);
       p.own_e = int(d.own0_end);
       p.nbands = int((l.n[2] + 63) / 64);
-      const long per_strip = long(p.n1) * p.nbands;
-      const long target = long(sm_count()) * 48;
-      int nstrips = int(std::max<long>(1, (target + per_strip / 2) / per_strip));
-      nstrips = std::min(nstrips, rows);
+      p.njg = int((l.n[1] + kRows3D - 1) / kRows3D);
+      p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
+      const bool recip = !var && p.kinv != 0.0;
+      const Kernel3D k3 = pick3d(var, nl, recip);
+      const long per_strip = long(p.njg) * p.nbands;
+      const long capacity = long(sm_count()) * k3.blocks_per_sm() * kWarps3D;
+      // strips: best fill of whole waves, discounting the 2 halo planes per strip
+      int nstrips = 1;
+      double best = -1.0;
+      for (int ns = 1; ns <= std::max(1, std::min(64, rows / 8)); ++ns) {
+        const long w = per_strip * ns;
+        const long waves = (w + capacity - 1) / capacity;
+        const double hh = double(rows) / ns;
+        const double eff = double(w) / double(waves * capacity) * hh / (hh + 2.0);
+        if (eff > best + 1e-9) {
+          best = eff;
+          nstrips = ns;
+        }
+      }
       p.H = (rows + nstrips - 1) / nstrips;
       p.nstrips = (rows + p.H - 1) / p.H;
       p.omega = weights[(first + k) % m];
       p.norms = d_norms + 2 * k;
       const long warps = per_strip * p.nstrips;
-      const long blocks = (warps + kWarps3D - 1) / kWarps3D;
-      if (var)
-        nl ? sweep3d<true, true><<<blocks, kWarps3D * 32, 0, st>>>(p)
-           : sweep3d<true, false><<<blocks, kWarps3D * 32, 0, st>>>(p);
-      else
-        nl ? sweep3d<false, true><<<blocks, kWarps3D * 32, 0, st>>>(p)
-           : sweep3d<false, false><<<blocks, kWarps3D * 32, 0, st>>>(p);
+      k3.launch(p, int((warps + kWarps3D - 1) / kWarps3D), st);
     }
     SRJ_CUDA(cudaGetLastError());
     k += t;

@@ -80,6 +80,41 @@ __device__ __forceinline__ void global_max(double *slot, double v) {
               static_cast<unsigned long long>(__double_as_longlong(v)));
 }
 
+// RN(a/c) for a fixed divisor c > 0 with y = RN(1/c), branch-free:
+// q0 = RN(a*y) is within 1.5 ulp of a/c; one Markstein correction
+// q1 = RN(q0 + RN(a - c*q0)*y) brings it within 1 ulp; with q1 faithful and y
+// within 1/2 ulp of 1/c, Markstein's theorem makes r1 = a - c*q1 exact and
+// RN(q1 + r1*y) = RN(a/c).  The sign is copied from a, which is exact for
+// c > 0 and restores IEEE's -0/c = -0.  Valid for a = +-0 and for normal a
+// with exponent in [-899, 899] (no overflow/underflow in q, r); other inputs
+// (subnormal, huge, inf, NaN) are flagged by recip_unsafe() and redone with
+// the IEEE division after a warp vote (see stage2d).
+__device__ __forceinline__ double div_recip(double a, double c, double y) {
+  double q = __dmul_rn(a, y);
+  double r = __fma_rn(-q, c, a);
+  q = __fma_rn(r, y, q);
+  r = __fma_rn(-q, c, a);
+  q = __fma_rn(r, y, q);
+  const int hi = (__double2hiint(q) & 0x7fffffff) | (__double2hiint(a) & int(0x80000000));
+  return __hiloint2double(hi, __double2loint(q));
+}
+
+__device__ __forceinline__ bool recip_unsafe(double a) {
+  const unsigned hi = unsigned(__double2hiint(a)) & 0x7fffffffu;
+  const unsigned e = hi >> 20;
+  const bool zero = (hi | unsigned(__double2loint(a))) == 0u;
+  return (e - 124u > 1798u) && !zero;  // exponent outside [-899, 899], nonzero
+}
+
+// out of line: the IEEE division is the rare path and its inline expansion
+// would triple the size of the unrolled fast loop
+__device__ __noinline__ double div_ieee(double a, double c) { return __ddiv_rn(a, c); }
+
+// keep the entry of larger magnitude (signed); NaN never replaces m
+__device__ __forceinline__ void acc_absmax(double &m, double x) {
+  m = (fabs(x) > fabs(m)) ? x : m;
+}
+
 // ---------------------------------------------------------------- mbarrier /
 // bulk-copy (TMA engine, non-tensor form) helpers
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {

@@ -1,12 +1,15 @@
 // srj_sweep3d.cuh -- 3D 7-point weighted-Jacobi sweep, the reference _wj3
 // (grids.py:379-408) restated for sm_100a.
 //
-// A warp owns one axis-1 row j and a 64-wide band of the contiguous axis 2; it
-// streams down axis 0 keeping u[i-1], u[i], u[i+1] of its row in registers
-// (each HBM byte of u read once per sweep), takes the k-1/k+1 neighbours by
-// warp shuffle (edge lanes load the band's outer neighbours) and the j-1/j+1
-// rows from L1/L2 (they are the neighbouring warps' streams, resident in the
-// same block).  The next row and its source are prefetched one tick ahead.
+// A warp owns J consecutive axis-1 rows j..j+J-1 and a 64-wide band of the
+// contiguous axis 2 (2 cells per lane); it streams down axis 0 keeping planes
+// i-1, i, i+1 of its rows in registers (each HBM byte of u read once per
+// sweep), takes k-1/k+1 by warp shuffle (edge lanes load the band's outer
+// neighbours), and reads only the two rows j-1 and j+J of plane i from L1/L2
+// (they are neighbouring warps' streams).  The next plane and its source are
+// prefetched one tick ahead.  Constant stencils divide with the branch-free
+// reciprocal refinement (div_recip, one warp vote per tick for IEEE fixups)
+// and derive dmax from rmax (monotone map), as the 2D kernel does.
 #pragma once
 #include "srj_device.cuh"
 
@@ -19,101 +22,158 @@ struct Sweep3DParams {
   const uint8_t *act;
   const double *coef[7];  // c, am0, ap0, am1, ap1, am2, ap2 (VAR)
   double kc[7];           // constant stencil
+  double kinv;            // RN(1/kc[0]) when the reciprocal path is used
   int64_t pitch, plane;
   int n0, n1, n2;
   int lo_c, hi_c, ld_lo, ld_hi, own_b, own_e;
-  int H, nbands, nstrips;
+  int H, nbands, nstrips, njg;
   double omega;
   double *norms;          // [2]
 };
 
-constexpr int kWarps3D = 8;
+constexpr int kWarps3D = 4;
+constexpr int kRows3D = 2;  // J: axis-1 rows per warp
 
-template <bool VAR, bool NL>
+template <bool VAR, bool NL, bool RECIP>
 __global__ void __launch_bounds__(kWarps3D * 32)
     sweep3d(const __grid_constant__ Sweep3DParams p) {
-  constexpr int V = 2, BAND = 64;  // cells per lane, cells per warp band
+  constexpr int V = 2, BAND = 64, J = kRows3D;  // cells per lane, cells per band
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const long gw = long(blockIdx.x) * kWarps3D + warp;
-  const int j = int(gw % p.n1);
-  const long rest = gw / p.n1;
+  const int jg = int(gw % p.njg);
+  const long rest = gw / p.njg;
   const int band = int(rest % p.nbands);
   const int strip = int(rest / p.nbands);
-  double dmx = 0.0, rmx = 0.0;
+  double rmx = 0.0, dmx = 0.0;
   if (strip < p.nstrips) {
     const int i0 = p.own_b + strip * p.H;
     const int i1 = min(i0 + p.H, p.own_e);
+    const int j0 = jg * J;
     const int col = band * BAND + V * lane;  // axis-2 index of this lane's first cell
     const bool in0 = col < p.n2, in1 = col + 1 < p.n2;
-    const int64_t jo = int64_t(j) * p.pitch + col;
-    auto U = [&](int i) { return p.src + int64_t(i) * p.plane + jo; };
+    const double *base = p.src + int64_t(j0) * p.pitch + col;  // plane 0, row j0
     auto ld2 = [](const double *a) { return __ldg(reinterpret_cast<const double2 *>(a)); };
-
-    double2 um = ld2(U(max(i0 - 1, p.ld_lo)));
-    double2 uc = ld2(U(i0));
-    double2 ud = ld2(U(min(i0 + 1, p.ld_hi)));
-    double2 fc = ld2(p.f + int64_t(i0) * p.plane + jo);
+    auto U = [&](int i, int q) { return base + int64_t(i) * p.plane + int64_t(q) * p.pitch; };
+    auto F = [&](int i, int q) {
+      return p.f + int64_t(min(max(i, p.lo_c), p.hi_c - 1)) * p.plane +
+             int64_t(j0 + q) * p.pitch + col;
+    };
+    double2 um[J], uc[J], ud[J], fc[J];
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+      um[q] = ld2(U(max(i0 - 1, p.ld_lo), q));
+      uc[q] = ld2(U(i0, q));
+      ud[q] = ld2(U(min(i0 + 1, p.ld_hi), q));
+      fc[q] = ld2(F(i0, q));
+    }
+    double *out = p.dst + int64_t(i0) * p.plane + int64_t(j0) * p.pitch + col;
 #pragma unroll 1
     for (int i = i0; i < i1; ++i) {
       // prefetch tick i+1
+      double2 udn[J], fcn[J];
       const int inext = min(i + 2, p.ld_hi);
-      const double2 ud_n = ld2(U(inext));
-      const double2 fc_n = ld2(p.f + int64_t(min(i + 1, p.hi_c - 1)) * p.plane + jo);
-      const double *row = U(i);
-      const double2 uN = ld2(row - p.pitch);
-      const double2 uS = ld2(row + p.pitch);
-      double west = __shfl_up_sync(kFull, uc.y, 1);
-      double east = __shfl_down_sync(kFull, uc.x, 1);
-      if (lane == 0) west = row[-1];
-      if (lane == 31) east = row[2];
+#pragma unroll
+      for (int q = 0; q < J; ++q) {
+        udn[q] = ld2(U(inext, q));
+        fcn[q] = ld2(F(i + 1, q));
+      }
+      const double2 nrow = ld2(U(i, -1));  // row j0-1 of plane i
+      const double2 srow = ld2(U(i, J));   // row j0+J of plane i
+      double west[J], east[J];
+#pragma unroll
+      for (int q = 0; q < J; ++q) {
+        west[q] = __shfl_up_sync(kFull, uc[q].y, 1);
+        east[q] = __shfl_down_sync(kFull, uc[q].x, 1);
+        if (lane == 0) west[q] = U(i, q)[-1];
+        if (lane == 31) east[q] = U(i, q)[2];
+      }
       const bool row_act = (i >= p.lo_c) && (i < p.hi_c);
-      const double ucv[2] = {uc.x, uc.y}, umv[2] = {um.x, um.y},
-                   udv[2] = {ud.x, ud.y}, nv[2] = {uN.x, uN.y},
-                   sv[2] = {uS.x, uS.y}, fv[2] = {fc.x, fc.y};
-      const double wv[2] = {west, uc.x}, ev[2] = {uc.y, east};
-      const bool inv[2] = {in0, in1};
-      double y[2];
+      double num[J][V], y[J][V];
+      bool actv[J][V];
+      bool bad = false;
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        bool act = row_act && inv[v];
-        double k[7];
-        if constexpr (VAR) {
-          const int64_t q = int64_t(i) * p.plane + jo + v;
+      for (int q = 0; q < J; ++q) {
+        const double2 nq = (q == 0) ? nrow : uc[q - 1];
+        const double2 sq = (q == J - 1) ? srow : uc[q + 1];
+        const double ucv[2] = {uc[q].x, uc[q].y}, umv[2] = {um[q].x, um[q].y},
+                     udv[2] = {ud[q].x, ud[q].y}, nv[2] = {nq.x, nq.y}, sv[2] = {sq.x, sq.y},
+                     fv[2] = {fc[q].x, fc[q].y};
+        const double wv[2] = {west[q], uc[q].x}, ev[2] = {uc[q].y, east[q]};
+        const bool rowq = row_act && (j0 + q < p.n1);
 #pragma unroll
-          for (int a = 0; a < 7; ++a) k[a] = __ldg(p.coef[a] + q);
-          if (p.act) act = act && (__ldg(p.act + q) != 0);
-        } else {
+        for (int v = 0; v < V; ++v) {
+          bool act = rowq && (v == 0 ? in0 : in1);
+          double k[7];
+          if (VAR) {
+            const int64_t o = int64_t(min(i, p.hi_c - 1)) * p.plane +
+                              int64_t(min(j0 + q, p.n1 - 1)) * p.pitch + col + v;
 #pragma unroll
-          for (int a = 0; a < 7; ++a) k[a] = p.kc[a];
-        }
-        const double s = NL ? nl_source(fv[v], ucv[v]) : fv[v];
-        const double rr = resid7(s, k[0], ucv[v], k[1], umv[v], k[2], udv[v],
-                                 k[3], nv[v], k[4], sv[v], k[5], wv[v], k[6], ev[v]);
-        const double d = relax(p.omega, rr, k[0]);
-        y[v] = act ? __dadd_rn(ucv[v], d) : ucv[v];
-        if (act) {
-          acc_max(dmx, d);
-          acc_max(rmx, rr);
+            for (int a = 0; a < 7; ++a) k[a] = __ldg(p.coef[a] + o);
+            if (p.act) act = act && (__ldg(p.act + o) != 0);
+          } else {
+#pragma unroll
+            for (int a = 0; a < 7; ++a) k[a] = p.kc[a];
+          }
+          const double s = NL ? nl_source(fv[v], ucv[v]) : fv[v];
+          const double rr = resid7(s, k[0], ucv[v], k[1], umv[v], k[2], udv[v], k[3], nv[v],
+                                   k[4], sv[v], k[5], wv[v], k[6], ev[v]);
+          double nm = __dmul_rn(p.omega, rr);
+          if (!act) nm = 1.0;  // keep garbage off the IEEE fixup path
+          double d;
+          if (RECIP) {
+            d = div_recip(nm, p.kc[0], p.kinv);
+            bad |= recip_unsafe(nm);
+          } else {
+            d = __ddiv_rn(nm, k[0]);
+          }
+          num[q][v] = nm;
+          actv[q][v] = act;
+          y[q][v] = act ? __dadd_rn(ucv[v], d) : ucv[v];
+          if (act) {
+            acc_absmax(rmx, rr);
+            if (VAR) acc_absmax(dmx, d);
+          }
         }
       }
-      double *o = p.dst + int64_t(i) * p.plane + jo;
-      if (in0 && in1) {
-        *reinterpret_cast<double2 *>(o) = make_double2(y[0], y[1]);
-      } else if (in0) {
-        o[0] = y[0];
+      if (RECIP && __any_sync(kFull, bad)) {
+#pragma unroll
+        for (int q = 0; q < J; ++q) {
+          const double ucv[2] = {uc[q].x, uc[q].y};
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            if (actv[q][v] && recip_unsafe(num[q][v]))
+              y[q][v] = __dadd_rn(ucv[v], div_ieee(num[q][v], p.kc[0]));
+        }
       }
-      um = uc;
-      uc = ud;
-      ud = ud_n;
-      fc = fc_n;
+#pragma unroll
+      for (int q = 0; q < J; ++q) {
+        if (j0 + q < p.n1) {
+          double *o = out + int64_t(q) * p.pitch;
+          if (in0 && in1) {
+            *reinterpret_cast<double2 *>(o) = make_double2(y[q][0], y[q][1]);
+          } else if (in0) {
+            o[0] = y[q][0];
+          }
+        }
+        um[q] = uc[q];
+        uc[q] = ud[q];
+        ud[q] = udn[q];
+        fc[q] = fcn[q];
+      }
+      out += p.plane;
     }
   }
-  dmx = warp_max(dmx);
-  rmx = warp_max(rmx);
+  const double rm = warp_max(fabs(rmx));
+  double dm;
+  if (VAR) {
+    dm = warp_max(fabs(dmx));
+  } else {
+    dm = fabs(__ddiv_rn(__dmul_rn(p.omega, rm), p.kc[0]));
+  }
   if (lane == 0) {
-    global_max(p.norms, dmx);
-    global_max(p.norms + 1, rmx);
+    global_max(p.norms, dm);
+    global_max(p.norms + 1, rm);
   }
 }
 
