@@ -25,7 +25,7 @@ import math
 import numpy as np
 
 __all__ = ["CONFIGS", "gaussian_sum", "poisson_fields", "nonlinear_fields",
-           "config_fields"]
+           "config_fields", "config_schedule"]
 
 # BASELINE.json configs -> (shape, P, table-N, source recipe)
 CONFIGS = {
@@ -37,9 +37,28 @@ CONFIGS = {
                  noise=False, width=(0.02, 0.08), seed=3),
     "cfg4": dict(shape=(32768, 32768), p=15, n_table=32768, n_gauss=32,
                  noise=True, width=(0.02, 0.1), seed=4),
-    "cfg5": dict(shape=(256, 256, 256), p=8, n_table=256, nonlinear=True,
+    # cfg5 uses the paper's effective-N route (srj/core.py:261-307, PAPER.md
+    # section 5.1): the 256^3 Dirichlet grid matches the 2-D Neumann table at
+    # N_eff = 181.7 -> the P=8 N=150 row.  The N=256 row diverges here: its
+    # transient amplification is fed back through the psi^5 source
+    # (profiles/round1_nl_schedules.log).
+    "cfg5": dict(shape=(256, 256, 256), p=8, n_table="effective", nonlinear=True,
                  seed=5),
 }
+
+
+def config_schedule(name, table=None):
+    """The CycleSchedule a BASELINE config runs (floor quantization)."""
+    from .schedule import effective_n, quantize
+    from .tables import shipped_table
+
+    cfg = CONFIGS[name]
+    table = table or shipped_table()
+    n = cfg["n_table"]
+    if n == "effective":
+        shape = cfg["shape"]
+        n = effective_n([s + 1 for s in shape], len(shape), "dirichlet")
+    return quantize(table.lookup(cfg["p"], int(n)))
 
 
 def _axes(shape):

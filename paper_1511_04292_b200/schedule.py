@@ -27,6 +27,7 @@ __all__ = [
     "DegenerateCycleError",
     "StabilityReport",
     "WeightSchedule",
+    "effective_n",
     "layout",
     "quantize",
     "validate_cycle",
@@ -191,3 +192,26 @@ def validate_cycle(cycle, kappa_range, grid_points=10000):
     amp = math.inf if top > 709 else math.exp(top)
     return StabilityReport(max_amplification=amp, kappa_at_max=float(grid[at]),
                            passed=amp < 1.0)
+
+
+def effective_n(sizes, d=None, bc="neumann"):
+    """2-D Neumann table size with the same kappa_min (``srj/core.py:261-307``).
+
+    Neumann:   n_eff = pi / (2 asin(sqrt(2/d) sin(pi/(2 n_max))))
+    Dirichlet: n_eff = pi / (2 asin(sqrt((2/d) sum_i sin(pi/(2 n_i))^2)))
+    """
+    s = np.atleast_1d(np.asarray(sizes, dtype=float))
+    if bool(np.any(s < 2)):
+        raise ValueError("all sizes must be >= 2")
+    d = int(s.size if d is None else d)
+    if d not in (1, 2, 3):
+        raise ValueError(f"d must be 1, 2 or 3, got {d}")
+    if bc == "neumann":
+        if d == 2:
+            return float(s.max())
+        arg = math.sqrt(2.0 / d) * math.sin(math.pi / (2.0 * s.max()))
+    elif bc == "dirichlet":
+        arg = math.sqrt((2.0 / d) * float(np.sum(np.sin(math.pi / (2.0 * s)) ** 2)))
+    else:
+        raise ValueError(f"unknown boundary kind {bc!r}")
+    return math.pi / (2.0 * math.asin(arg))

@@ -84,3 +84,14 @@ def test_weight_schedule_validation():
         WeightSchedule([1.0, 2.0], [0.5, 0.5], 10)
     with pytest.raises(ValueError, match="sum to 1"):
         WeightSchedule([5.0, 0.5], [0.5, 0.6], 10)
+
+
+def test_effective_n_matches_reference_examples():
+    from paper_1511_04292_b200.problems import config_schedule
+    from paper_1511_04292_b200.schedule import effective_n
+
+    # test_core.py:227-230 / core.py docstring: 585 x 280 Dirichlet -> 252.56
+    assert round(effective_n((585, 280), bc="dirichlet"), 2) == 252.56
+    assert abs(effective_n((257, 257, 257), 3, "dirichlet") - 181.73) < 0.01
+    assert config_schedule("cfg5").source_schedule.n == 150
+    assert config_schedule("cfg2").m == 25530
