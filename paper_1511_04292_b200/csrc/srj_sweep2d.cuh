@@ -197,12 +197,14 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
                const __grid_constant__ CUtensorMap tm_f) {
   using B = Band2D<T, V>;
   constexpr int BAND = B::BAND, TP = B::TP, OWN = B::OWN, NS = B::NS, G = B::G, LAG = B::LAG;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char *smem = reinterpret_cast<unsigned char *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // dynamic shared memory starts the CTA's shared window (no static smem), so
+  // it is 1024-byte aligned; indexing the symbol directly keeps every ring
+  // access an LDS (pointer arithmetic through integers would turn them into
+  // generic loads)
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  unsigned char *wbase = smem + size_t(warp) * B::WARP_BYTES;
+  unsigned char *wbase = smem_raw + size_t(warp) * B::WARP_BYTES;
   double *ring = reinterpret_cast<double *>(wbase);  // slot s: u box, then source box
   uint64_t *bars = reinterpret_cast<uint64_t *>(wbase + NS * B::SLOT_BYTES);
 
