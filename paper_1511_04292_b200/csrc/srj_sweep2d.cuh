@@ -67,13 +67,13 @@ struct Band2D {
   static constexpr int OWN = BAND - 2 * TP;      // columns a band owns
   static constexpr int G = 3;                    // rows per TMA group
   static constexpr int LAG = (2 * T + G - 1) / G;  // groups a source row stays live
-  static constexpr int NS = (LAG + 5 <= 8) ? 8 : 16;  // ring slots (power of 2)
-  static constexpr int LOG_NS = (NS == 8) ? 3 : 4;
+  static constexpr int NU = 4;                      // u-box slots: prefetch NU-1 groups
+  static constexpr int NF = (NU + LAG <= 8) ? 8 : 16;  // source slots >= NU + LAG
+  static constexpr int LOG_NF = (NF == 8) ? 3 : 4;
   static constexpr int WARPS = 2;
   static constexpr int BOX_BYTES = G * BAND * 8;      // one array, one group
-  static constexpr int SLOT_BYTES = 2 * BOX_BYTES;    // u box + source box
-  static constexpr int WARP_BYTES = (NS * SLOT_BYTES + NS * 8 + 127) / 128 * 128;
-  static constexpr size_t smem_bytes() { return size_t(WARPS) * WARP_BYTES + 128; }
+  static constexpr int WARP_BYTES = ((NU + NF) * BOX_BYTES + NF * 8 + 127) / 128 * 128;
+  static constexpr size_t smem_bytes() { return size_t(WARPS) * WARP_BYTES; }
 };
 
 
@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
     sweep2d_tb(const __grid_constant__ Sweep2DParams p, const __grid_constant__ CUtensorMap tm_u,
                const __grid_constant__ CUtensorMap tm_f) {
   using B = Band2D<T, V>;
-  constexpr int BAND = B::BAND, TP = B::TP, OWN = B::OWN, NS = B::NS, G = B::G, LAG = B::LAG;
+  constexpr int BAND = B::BAND, TP = B::TP, OWN = B::OWN, NU = B::NU, NF = B::NF, G = B::G;
+  constexpr int BOXD = B::BOX_BYTES / 8;  // doubles per box
   // dynamic shared memory starts the CTA's shared window (no static smem), so
   // it is 1024-byte aligned; indexing the symbol directly keeps every ring
   // access an LDS (pointer arithmetic through integers would turn them into
@@ -205,8 +206,9 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   unsigned char *wbase = smem_raw + size_t(warp) * B::WARP_BYTES;
-  double *ring = reinterpret_cast<double *>(wbase);  // slot s: u box, then source box
-  uint64_t *bars = reinterpret_cast<uint64_t *>(wbase + NS * B::SLOT_BYTES);
+  double *ring_u = reinterpret_cast<double *>(wbase);  // NU u boxes
+  double *ring_f = ring_u + NU * BOXD;                   // NF source boxes
+  uint64_t *bars = reinterpret_cast<uint64_t *>(ring_f + NF * BOXD);  // one per group mod NF
 
   const int gw = blockIdx.x * B::WARPS + warp;
   const int band = gw % p.nbands;
@@ -239,22 +241,24 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
   const int tma_col = p.tma_col0 + col_band;
   const int tma_row = p.tma_row0 + rho_b;
 
+  // group g: u box -> ring_u[g mod NU], source box -> ring_f[g mod NF], both
+  // completing on bars[g mod NF].  Issued at the end of group g-NU, when the
+  // u slot is free; the source slot is free too because NF >= NU + LAG.
   auto issue = [&](int g) {
-    const int s = g & (NS - 1);
-    double *slot = ring + s * (B::SLOT_BYTES / 8);
-    mbar_expect_tx(&bars[s], B::SLOT_BYTES);
-    tma_load_2d(slot, &tm_u, tma_col, tma_row + G * g, &bars[s]);
-    tma_load_2d(slot + G * BAND, &tm_f, tma_col, tma_row + G * g, &bars[s]);
+    uint64_t *bar = &bars[g & (NF - 1)];
+    mbar_expect_tx(bar, 2 * B::BOX_BYTES);
+    tma_load_2d(ring_u + (g & (NU - 1)) * BOXD, &tm_u, tma_col, tma_row + G * g, bar);
+    tma_load_2d(ring_f + (g & (NF - 1)) * BOXD, &tm_f, tma_col, tma_row + G * g, bar);
   };
 
   if (lane == 0) {
     tma_prefetch_desc(&tm_u);
     tma_prefetch_desc(&tm_f);
 #pragma unroll 1
-    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NF; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
 #pragma unroll 1
-    for (int g = 0; g < NS && g < ngroups; ++g) issue(g);
+    for (int g = 0; g < NU && g < ngroups; ++g) issue(g);
   }
   __syncwarp();
 
@@ -273,8 +277,7 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
 
 #pragma unroll 1
   for (int g = 0; g < ngroups; ++g) {
-    const int s = g & (NS - 1);
-    mbar_wait(&bars[s], (g >> B::LOG_NS) & 1);
+    mbar_wait(&bars[g & (NF - 1)], (g >> B::LOG_NF) & 1);
 #pragma unroll
     for (int ph = 0; ph < G; ++ph) {
       const int it = G * g + ph;
@@ -288,8 +291,7 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
   _Pragma("unroll") for (int t = T; t >= 1; --t) {                                            \
     const int fg = g + ((ph - 2 * t) >= 0 ? 0 : -((2 * t - ph + G - 1) / G));                 \
     const int fr = ph - 2 * t + G * (g - fg);                                                 \
-    const double *frow = ring + (fg & (NS - 1)) * (B::SLOT_BYTES / 8) + G * BAND + fr * BAND + \
-                         V * lane;                                                            \
+    const double *frow = ring_f + (fg & (NF - 1)) * BOXD + fr * BAND + V * lane;              \
     double(&dst)[V] = (t == T) ? yT : w[t + 1][ph % 3];                                       \
     stage2d<FASTV, EDGEV, VAR, NL, RECIP, V>(p, w[t][ph % 3], w[t][(ph + 1) % 3],            \
                                       w[t][(ph + 2) % 3], frow, rho - 2 * t, p.omega[t - 1],  \
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
       }
 #undef SRJ_STAGE
       {  // stage 0: the freshly loaded row enters stage 1's window
-        const double *urow = ring + s * (B::SLOT_BYTES / 8) + ph * BAND + V * lane;
+        const double *urow = ring_u + (g & (NU - 1)) * BOXD + ph * BAND + V * lane;
 #pragma unroll
         for (int v = 0; v < V; v += 2) {
           const double2 q = *reinterpret_cast<const double2 *>(urow + v);
@@ -337,9 +339,9 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
       out += p.pitch;
     }
     __syncwarp();
-    if (lane == 0 && g >= LAG && g - LAG + NS < ngroups) {
+    if (lane == 0 && g + NU < ngroups) {
       fence_proxy_async();
-      issue(g - LAG + NS);
+      issue(g + NU);
     }
   }
 
