@@ -73,6 +73,16 @@ int waves_2d() {
   return w;
 }
 
+// SRJ_BPS=<n>: size the 2D grid for n resident blocks per SM (tuning knob)
+int bps_override() {
+  static int b = -1;
+  if (b < 0) {
+    const char *e = getenv("SRJ_BPS");
+    b = e ? atoi(e) : 0;
+  }
+  return b;
+}
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -424,7 +434,9 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       const Kernel2D k2 = pick2d(t, var, nl, !var && p.kinv != 0.0);
       p.nbands = int((l.n[1] + k2.own - 1) / k2.own);
       // strips x bands = waves x resident warps (default one wave)
-      const int capacity = sm_count() * k2.blocks_per_sm() * Band2D<1, 2>::WARPS * waves_2d();
+      const int bps = bps_override() > 0 ? std::min(bps_override(), k2.blocks_per_sm())
+                                         : k2.blocks_per_sm();
+      const int capacity = sm_count() * bps * Band2D<1, 2>::WARPS * waves_2d();
       int nstrips = std::max(1, capacity / p.nbands);
       nstrips = std::min(nstrips, std::max(1, rows / std::max(2 * t, 8)));
       p.H = (rows + nstrips - 1) / nstrips;
