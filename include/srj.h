@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SRJ_ABI_VERSION 1
+#define SRJ_ABI_VERSION 2
 
 enum {
     SRJ_OK = 0,
@@ -92,6 +92,20 @@ int srj_wj_dense(int32_t ndim, const int64_t *n, const double *u, double *un,
  * Solver plan: the device side of srj_solve / jacobi_solve / _Sweeper
  * (grids.py:535-559, :602-694).  Buffers are owned by the caller.
  * ---------------------------------------------------------------------- */
+enum {
+    SRJ_BC_FIXED = 0,          /* ghosts never touched                       */
+    SRJ_BC_MIRROR = 1,         /* ghost = adjacent interior cell              */
+    SRJ_BC_PERIODIC = 2,       /* ghost = interior cell at the opposite face  */
+    SRJ_BC_FACE_DIRICHLET = 3  /* ghost = 2*value - adjacent interior cell    */
+};
+
+typedef struct {
+    int32_t kind;              /* SRJ_BC_*                                    */
+    double value;              /* face_dirichlet scalar (when values == NULL) */
+    const double *values;      /* face_dirichlet: device array, dense, shaped
+                                  like the interior without this axis         */
+} srj_face_rule;
+
 typedef struct {
     srj_layout_t layout;         /* from srj_layout()                         */
     int32_t coef_mode;           /* 0: constant stencil (scalars below)       */
@@ -108,6 +122,11 @@ typedef struct {
     int64_t own0_end;            /*   stores and norms (default 0, n[0])      */
     int32_t physical_lo0;        /* 1: layer below row 0 is a FIXED boundary  */
     int32_t physical_hi0;        /* 1: layer above row n0-1 is a FIXED bound. */
+    srj_face_rule bc[3][2];      /* per axis (low, high) ghost rule; all-zero =
+                                    FIXED everywhere.  Any non-FIXED face runs
+                                    one sweep per launch followed by the ghost
+                                    refresh (BoundaryRule, grids.py:73-112,
+                                    refresh_ghosts :225-247); single-slab only */
 } srj_plan_desc;
 
 typedef struct srj_plan srj_plan;

@@ -13,8 +13,10 @@ from .oracle import (  # noqa: F401
     OVERFLOW_LIMIT,
     load,
     np_step,
+    refresh_ghosts,
     residual,
     run,
+    run_bc,
     solve,
     step,
 )

@@ -253,3 +253,59 @@ def solve(problem, weights, tol, max_iters=10_000_000, rule="update_inf",
                 break
     norms = np.concatenate(all_norms) if all_norms else np.zeros((0, 2))
     return done, status, norms, checks
+
+
+def refresh_ghosts(u, bc):
+    """Ghost refresh of ``GridProblem.refresh_ghosts`` (grids.py:225-247).
+
+    ``bc``: per axis (lo, hi) pairs of (kind, values) with kind in
+    fixed/mirror/periodic/face_dirichlet.  Faces write only their ghost layer
+    with the other axes interior; face_dirichlet = 2*values - interior.
+    """
+    nd = u.ndim
+
+    def face(ax, pos):
+        idx = [slice(1, -1)] * nd
+        idx[ax] = pos
+        return tuple(idx)
+
+    for ax in range(nd):
+        n = u.shape[ax]
+        (klo, vlo), (khi, vhi) = bc[ax]
+        if klo == "mirror":
+            u[face(ax, 0)] = u[face(ax, 1)]
+        elif klo == "periodic":
+            u[face(ax, 0)] = u[face(ax, n - 2)]
+        elif klo == "face_dirichlet":
+            u[face(ax, 0)] = 2.0 * vlo - u[face(ax, 1)]
+        if khi == "mirror":
+            u[face(ax, n - 1)] = u[face(ax, n - 2)]
+        elif khi == "periodic":
+            u[face(ax, n - 1)] = u[face(ax, 1)]
+        elif khi == "face_dirichlet":
+            u[face(ax, n - 1)] = 2.0 * vhi - u[face(ax, n - 2)]
+
+
+def run_bc(problem, bc, weights, nsteps, tol=0.0, kappa=None):
+    """Step-by-step solve with a ghost refresh after every step (any bc).
+
+    Same stopping semantics as ``run`` (grids.py:613-628); returns
+    (steps, status, norms[steps, 2]).
+    """
+    w = np.asarray(weights, dtype=np.float64)
+    norms = []
+    status = 0
+    for k in range(int(nsteps)):
+        omega = w[k % len(w)]
+        dm, rm = step(problem, omega, kappa=kappa)
+        refresh_ghosts(problem.u, bc)
+        norms.append((dm, rm))
+        if tol != 0.0:
+            metric = dm / abs(omega)
+            if not np.isfinite(metric) or metric > OVERFLOW_LIMIT:
+                status = 2
+                break
+            if tol > 0.0 and metric < tol:
+                status = 1
+                break
+    return len(norms), status, np.asarray(norms).reshape(-1, 2)

@@ -8,7 +8,7 @@ build command.  ``load()`` is the single gate.
 import ctypes
 import os
 
-__all__ = ["LIB_PATH", "SrjLayout", "SrjPlanDesc", "check", "load"]
+__all__ = ["BC_KINDS", "LIB_PATH", "SrjFaceRule", "SrjLayout", "SrjPlanDesc", "check", "load"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsrj.so")
 
@@ -17,7 +17,9 @@ SRJ_EINVAL = -1
 SRJ_ECUDA = -2
 SRJ_ENOMEM = -3
 SRJ_EUNSUPPORTED = -4
-ABI_VERSION = 1
+ABI_VERSION = 2
+
+BC_KINDS = {"fixed": 0, "mirror": 1, "periodic": 2, "face_dirichlet": 3}
 
 _c_dp = ctypes.POINTER(ctypes.c_double)
 
@@ -35,6 +37,14 @@ class SrjLayout(ctypes.Structure):
     ]
 
 
+class SrjFaceRule(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("value", ctypes.c_double),
+        ("values", ctypes.c_void_p),
+    ]
+
+
 class SrjPlanDesc(ctypes.Structure):
     _fields_ = [
         ("layout", SrjLayout),
@@ -48,6 +58,7 @@ class SrjPlanDesc(ctypes.Structure):
         ("own0_end", ctypes.c_int64),
         ("physical_lo0", ctypes.c_int32),
         ("physical_hi0", ctypes.c_int32),
+        ("bc", (SrjFaceRule * 2) * 3),
     ]
 
 

@@ -232,6 +232,7 @@ __global__ void selftest_div(const double *a, int64_t n, double c, double y, dou
 
 struct srj_plan {
   srj_plan_desc d;
+  bool has_bc;       // some face is not FIXED: refresh ghosts after each sweep
   int default_fuse;
   double *partials;  // [kResidBlocks][2] device scratch
 };
@@ -330,7 +331,28 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
     delete p;
     return fail(SRJ_EINVAL, "owned rows out of range");
   }
-  p->default_fuse = (l.ndim == 2 && desc->coef_mode == 0) ? 4 : 1;
+  p->has_bc = false;
+  for (int a = 0; a < 3; ++a)
+    for (int side = 0; side < 2; ++side) {
+      const int k = desc->bc[a][side].kind;
+      if (k < SRJ_BC_FIXED || k > SRJ_BC_FACE_DIRICHLET || (k != SRJ_BC_FIXED && a >= l.ndim)) {
+        delete p;
+        return fail(SRJ_EINVAL, "bad boundary rule on axis %d", a);
+      }
+      if (k != SRJ_BC_FIXED) p->has_bc = true;
+    }
+  for (int a = 0; a < l.ndim; ++a)
+    if ((desc->bc[a][0].kind == SRJ_BC_PERIODIC) != (desc->bc[a][1].kind == SRJ_BC_PERIODIC)) {
+      delete p;
+      return fail(SRJ_EINVAL, "periodic axes need the rule on both faces");
+    }
+  if (p->has_bc && (!desc->physical_lo0 || !desc->physical_hi0 || p->d.own0_begin != 0 ||
+                    p->d.own0_end != l.n[0])) {
+    delete p;
+    return fail(SRJ_EUNSUPPORTED, "non-FIXED boundary rules need the whole grid on one plan");
+  }
+  // non-FIXED ghosts change every step: one sweep per launch + refresh
+  p->default_fuse = (l.ndim == 2 && desc->coef_mode == 0 && !p->has_bc) ? 4 : 1;
   p->partials = nullptr;
   cudaError_t e = cudaMalloc(&p->partials, sizeof(double) * 2 * kResidBlocks);
   if (e != cudaSuccess) {
@@ -367,6 +389,33 @@ static void row_ranges(const srj_plan_desc &d, int &lo_c, int &hi_c, int &ld_lo,
   }
 }
 
+static int launch_ghosts(const srj_plan_desc &d, double *u0, cudaStream_t st) {
+  const srj_layout_t &l = d.layout;
+  GhostParams g{};
+  g.u = u0;
+  g.ndim = l.ndim;
+  g.stride[l.ndim - 1] = 1;
+  g.stride[l.ndim - 2] = l.pitch;
+  if (l.ndim == 3) g.stride[0] = l.plane;
+  for (int a = 0; a < 3; ++a) g.n[a] = a < l.ndim ? int(l.n[a]) : 1;
+  g.face_start[0] = 0;
+  for (int f = 0; f < 2 * l.ndim; ++f) {
+    const int ax = f >> 1, side = f & 1;
+    int64_t size = 1;
+    for (int a = 0; a < l.ndim; ++a)
+      if (a != ax) size *= l.n[a];
+    g.face_start[f + 1] = g.face_start[f] + size;
+    g.kind[ax][side] = d.bc[ax][side].kind;
+    g.value[ax][side] = d.bc[ax][side].value;
+    g.values[ax][side] = d.bc[ax][side].values;
+  }
+  const int64_t total = g.face_start[2 * l.ndim];
+  const int blocks = int(std::min<int64_t>((total + 255) / 256, int64_t(sm_count()) * 4));
+  ghost_refresh<<<std::max(blocks, 1), 256, 0, st>>>(g);
+  SRJ_CUDA(cudaGetLastError());
+  return SRJ_OK;
+}
+
 int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b,
                  const double *weights, int64_t m, int64_t first, int64_t nsteps, int32_t fuse,
                  double *d_norms, int32_t *final_buf, void *stream) {
@@ -383,7 +432,7 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
   const srj_layout_t &l = d.layout;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int T = fuse > 0 ? fuse : plan->default_fuse;
-  if (l.ndim == 3) T = 1;
+  if (l.ndim == 3 || plan->has_bc) T = 1;
   if (T > kMaxFuse) return fail(SRJ_EINVAL, "fuse depth %d exceeds %d", T, kMaxFuse);
   if ((!d.physical_lo0 || !d.physical_hi0) && T > l.halo0)
     return fail(SRJ_EINVAL, "fuse depth %d needs halo0 >= %d on exchanged faces", T, T);
@@ -503,6 +552,10 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       k3.launch(p, int((warps + kWarps3D - 1) / kWarps3D), st);
     }
     SRJ_CUDA(cudaGetLastError());
+    if (plan->has_bc) {
+      const int rc = launch_ghosts(d, nxt + ioff, st);
+      if (rc != SRJ_OK) return rc;
+    }
     k += t;
     *final_buf = which;
     cur = nxt;

@@ -113,6 +113,57 @@ __global__ void __launch_bounds__(32) residual_final(const double *partials, int
   }
 }
 
+// Ghost-layer refresh after a sweep: GridProblem.refresh_ghosts
+// (grids.py:225-247).  Every face writes only its ghost layer with the other
+// axes restricted to the interior (corners untouched, as the reference) and
+// reads only interior cells, so the faces are independent.  face_dirichlet is
+// RN(RN(2*v) - u) like numpy's `2.0 * values - u[...]`.
+struct GhostParams {
+  double *u;              // interior origin of the buffer to refresh
+  int64_t stride[3];      // element stride per axis (padded layout)
+  int n[3];               // interior extents (unused axes = 1)
+  int ndim;
+  int kind[3][2];
+  double value[3][2];
+  const double *values[3][2];
+  int64_t face_start[7];  // prefix sums of face sizes over the 2*ndim faces
+};
+
+__global__ void __launch_bounds__(256) ghost_refresh(const __grid_constant__ GhostParams p) {
+  const int nf = 2 * p.ndim;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < p.face_start[nf];
+       q += int64_t(gridDim.x) * blockDim.x) {
+    int f = 0;
+    while (q >= p.face_start[f + 1]) ++f;
+    const int ax = f >> 1, side = f & 1;
+    const int kind = p.kind[ax][side];
+    if (kind == 0) continue;
+    int64_t rem = q - p.face_start[f];
+    // position along the other axes (C order, interior indices)
+    int64_t off = 0;
+    for (int a = p.ndim - 1; a >= 0; --a) {
+      if (a == ax) continue;
+      const int64_t idx = rem % p.n[a];
+      rem /= p.n[a];
+      off += idx * p.stride[a];
+    }
+    const int64_t sa = p.stride[ax];
+    const int64_t ghost = off + (side ? int64_t(p.n[ax]) : -1) * sa;
+    const int64_t adj = off + (side ? int64_t(p.n[ax] - 1) : 0) * sa;
+    double g;
+    if (kind == 1) {
+      g = p.u[adj];
+    } else if (kind == 2) {
+      g = p.u[off + (side ? 0 : int64_t(p.n[ax] - 1)) * sa];
+    } else {
+      const double v = p.values[ax][side] ? p.values[ax][side][q - p.face_start[f]]
+                                          : p.value[ax][side];
+      g = __dsub_rn(__dmul_rn(2.0, v), p.u[adj]);
+    }
+    p.u[ghost] = g;
+  }
+}
+
 struct DenseParams {
   const double *u;
   double *un;

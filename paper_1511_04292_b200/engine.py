@@ -64,7 +64,7 @@ class DeviceGrid:
     """
 
     def __init__(self, u, source, center, lower, upper, active=None, kappa=None,
-                 halo0=1, own=None, physical=(True, True), device=None):
+                 halo0=1, own=None, physical=(True, True), device=None, bc=None):
         torch = require_cuda()
         lib = _lib.load()
         self.torch = torch
@@ -120,6 +120,9 @@ class DeviceGrid:
             desc.own0_end = int(hi)
             desc.physical_lo0 = int(bool(physical[0]))
             desc.physical_hi0 = int(bool(physical[1]))
+            for ax, pair in enumerate(bc or ()):
+                for side, rule in enumerate(pair):
+                    self._set_face(desc.bc[ax][side], rule, ax)
             self.desc = desc
             plan = ctypes.c_void_p()
             _lib.check(lib.srj_plan_create(ctypes.byref(desc), ctypes.byref(plan)),
@@ -127,6 +130,21 @@ class DeviceGrid:
             self.plan = plan
             self.norms = torch.zeros(2, dtype=torch.float64, device=self.device)
             self.resid_out = torch.zeros(2, dtype=torch.float64, device=self.device)
+
+    def _set_face(self, face, rule, ax):
+        """Fill one srj_face_rule from a reference BoundaryRule (grids.py:73-112)."""
+        face.kind = _lib.BC_KINDS[rule.kind]
+        if rule.kind != "face_dirichlet":
+            return
+        vals = np.asarray(rule.values, dtype=np.float64)
+        face_shape = self.shape[:ax] + self.shape[ax + 1:]
+        if vals.ndim == 0:
+            face.value = float(vals)
+            return
+        dense = np.ascontiguousarray(np.broadcast_to(vals, face_shape))
+        t = self.torch.from_numpy(dense.copy()).to(self.device)
+        self._keep.append(t)
+        face.values = t.data_ptr()
 
     # ------------------------------------------------------------- transfers
     @property

@@ -8,10 +8,12 @@ module's look-alikes: any object with the ``GridProblem`` attributes
 ``_active``, ``post_sweep``) and any cycle with ``weight_sequence``.
 
 GPU scope: 2-D 5-point and 3-D 7-point stencils with
-FIXED ghost layers (point-centred Dirichlet data), constant or per-cell
-coefficients, optional mask, optional nonlinear source.  Other boundary rules,
-``post_sweep`` hooks, 1-D grids and the Gauss-Seidel/SOR solvers raise
-``NotImplementedError`` -- there is no CPU fallback.
+every reference boundary rule (FIXED ghosts run fused multi-sweep kernels;
+mirror / periodic / face-Dirichlet faces run one sweep per launch followed by
+a device ghost refresh), constant or per-cell coefficients, optional mask,
+optional nonlinear source.  ``post_sweep`` hooks (arbitrary Python), 1-D grids
+and the Gauss-Seidel/SOR solvers raise ``NotImplementedError`` -- there is no
+CPU fallback.
 
 Entry points and the reference code they replace:
 
@@ -269,9 +271,8 @@ def _device_grid(problem):
         raise NotImplementedError("the GPU path supports 2- and 3-dimensional grids")
     for pair in problem.bc:
         for rule in pair:
-            if rule.kind != "fixed":
-                raise NotImplementedError(
-                    f"boundary kind {rule.kind!r} is not on the GPU path (FIXED only)")
+            if rule.kind not in ("fixed", "mirror", "periodic", "face_dirichlet"):
+                raise NotImplementedError(f"boundary kind {rule.kind!r} is not on the GPU path")
     if getattr(problem, "post_sweep", None) is not None:
         raise NotImplementedError("post_sweep hooks are not on the GPU path")
     active = getattr(problem, "_active", None)
@@ -279,7 +280,7 @@ def _device_grid(problem):
         active = getattr(problem, "mask", None)
     kappa = getattr(problem, "source_kappa", None)
     return DeviceGrid(problem.u, problem.source, problem.center, problem.lower,
-                      problem.upper, active=active, kappa=kappa)
+                      problem.upper, active=active, kappa=kappa, bc=problem.bc)
 
 
 def _step_seconds_estimate(problem):

@@ -39,3 +39,31 @@ def fields_from(g):
 @pytest.fixture
 def golden():
     return load_golden
+
+
+def bc_from(g):
+    """Boundary spec stored in a golden fixture: per axis ((kind, values), ...)."""
+    nd = g["source"].ndim
+    out = []
+    for ax in range(nd):
+        pair = []
+        for side in range(2):
+            kind = str(g[f"bc{ax}{side}"]) if f"bc{ax}{side}" in g else "fixed"
+            vals = g.get(f"bcval{ax}{side}")
+            pair.append((kind, vals))
+        out.append(tuple(pair))
+    return tuple(out)
+
+
+def rules_from(g):
+    """The same spec as this package's BoundaryRule objects."""
+    from paper_1511_04292_b200 import grids as G
+
+    out = []
+    for pair in bc_from(g):
+        rules = []
+        for kind, vals in pair:
+            rules.append(G.face_dirichlet(vals) if kind == "face_dirichlet"
+                         else G.BoundaryRule(kind))
+        out.append(tuple(rules))
+    return tuple(out)

@@ -110,6 +110,7 @@ def test_unsupported_features_raise():
     with pytest.raises(NotImplementedError):
         G.srj_solve(p, type("C", (), {"weight_sequence": np.ones(1)})(), 1e-6)
     q = G.GridProblem(**_kw((4, 4), bc=((G.MIRROR, G.MIRROR),) * 2))
+    q.post_sweep = lambda u: None
     with pytest.raises(NotImplementedError):
         G.jacobi_solve(q, 1e-6)
     with pytest.raises(NotImplementedError):

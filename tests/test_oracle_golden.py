@@ -110,3 +110,22 @@ def test_oracle_nonlinear_source_restatement():
     c = problem_from(f)
     oracle.run(c, w, 0, len(w), kappa=f["kappa"])
     assert oracle.residual(c, kappa=f["kappa"])[0] < r0
+
+
+BC_CASES = ["neumann2d", "periodic2d", "facedir3d", "gs_a", "gs_b", "gs_a_solve"]
+
+
+@pytest.mark.parametrize("name", BC_CASES)
+def test_oracle_boundary_rules_match_reference(name):
+    from conftest import bc_from
+
+    g = load_golden(name)
+    p = problem_from(fields_from(g))
+    steps, status, norms = oracle.run_bc(p, bc_from(g), g["weights"], int(g["steps"]),
+                                         tol=float(g["tol"]))
+    assert steps == len(g["residual_inf"])
+    assert status == (1 if bool(g["converged"]) else 0)
+    assert np.array_equal(p.u, g["u_final"])
+    metric = norms[:, 0] / np.abs(g["weights"][np.arange(steps) % len(g["weights"])])
+    assert np.array_equal(metric, g["residual_inf"])
+    assert np.array_equal(norms[:, 1], g["true_residual_inf"])

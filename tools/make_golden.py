@@ -188,6 +188,76 @@ def main():
                           width=(0.02, 0.08))
     fixed_steps("const3d_p6", c3, w64, 300)
 
+    # ---- non-FIXED boundary rules (BoundaryRule, grids.py:73-112) ---------
+    from srj.problems import grad_shafranov, laplace2d_neumann
+
+    def bc_fixture(name, prob, weights, steps, tol=1e-300):
+        """Run the reference srj_solve on a full GridProblem (any bc)."""
+        nd = prob.ndim
+        arr = {"u0": prob.u.copy(), "source": prob.source.copy(),
+               "center": prob.center.copy()}
+        for ax in range(nd):
+            arr[f"lower{ax}"] = prob.lower[ax].copy()
+            arr[f"upper{ax}"] = prob.upper[ax].copy()
+            for side in range(2):
+                rule = prob.bc[ax][side]
+                arr[f"bc{ax}{side}"] = np.array(rule.kind)
+                if rule.kind == "face_dirichlet":
+                    arr[f"bcval{ax}{side}"] = np.asarray(rule.values, dtype=float)
+        if prob.mask is not None:
+            arr["mask"] = prob.mask.copy()
+
+        class _Cycle:
+            weight_sequence = np.asarray(weights, dtype=float)
+
+        hist, _ = G.srj_solve(prob, _Cycle(), tol=tol, max_iters=steps)
+        arr.update(weights=np.asarray(weights, dtype=float), steps=np.int64(steps),
+                   tol=np.float64(tol), u_final=prob.u, residual_inf=hist.residual_inf,
+                   true_residual_inf=hist.true_residual_inf,
+                   converged=np.bool_(hist.converged))
+        save(name, **arr)
+
+    nm = laplace2d_neumann(24)
+    nm.u[1:-1, 1:-1] = np.random.default_rng(3).standard_normal(nm.shape)
+    nm.refresh_ghosts()
+    bc_fixture("neumann2d", nm, w64, 200)
+
+    f = random_fields(rng, (20, 26), False)
+    per = G.GridProblem(spacing=(1.0, 1.0), u=f["u"], source=f["source"],
+                        center=f["center"], lower=f["lower"], upper=f["upper"],
+                        bc=((G.FIXED, G.FIXED), (G.PERIODIC, G.PERIODIC)))
+    bc_fixture("periodic2d", per, w64, 150)
+
+    f = random_fields(rng, (9, 11, 12), True)
+    fd = G.GridProblem(
+        spacing=(1.0,) * 3, u=f["u"], source=f["source"], center=f["center"],
+        lower=f["lower"], upper=f["upper"], mask=f["mask"],
+        bc=((G.face_dirichlet(rng.standard_normal((11, 12))), G.MIRROR),
+            (G.PERIODIC, G.PERIODIC),
+            (G.face_dirichlet(0.75), G.face_dirichlet(rng.standard_normal((9, 11))))))
+    bc_fixture("facedir3d", fd, w64, 120)
+
+    bc_fixture("gs_a", grad_shafranov("A", 0.0, 40), w64, 300)
+    bc_fixture("gs_b", grad_shafranov("B", 0.0, 48), w64, 300)
+    gs_row = table.lookup(14, 300)
+    bc_fixture("gs_a_solve", grad_shafranov("A", 0.0, 60),
+               quantize(gs_row).weight_sequence,
+               200_000, tol=1e-10)
+
+    # builder pins for the restated Grad-Shafranov / Neumann problems
+    pins = {}
+    for test, c, n in (("A", 0.0, 40), ("A", 0.34, 33), ("B", 0.0, 48)):
+        p = grad_shafranov(test, c, n)
+        tag = f"gs_{test}_{str(c).replace('.', 'p')}_{n}"
+        pins[tag + "_u"] = p.u
+        pins[tag + "_center"] = p.center
+        pins[tag + "_lower1"] = p.lower[1]
+        pins[tag + "_upper1"] = p.upper[1]
+        pins[tag + "_lower0"] = p.lower[0]
+        if p.mask is not None:
+            pins[tag + "_mask"] = p.mask
+    save("builders", **pins)
+
     # ---- divergence (test_grids.py:421-432 on a FIXED-ghost problem) -----
     bad = quantize(WeightSchedule(omegas=[50.0, 0.5], betas=[0.5, 0.5], n=64))
     dv = random_fields(rng, (24, 24), False)
