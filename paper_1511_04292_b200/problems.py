@@ -138,6 +138,71 @@ def nonlinear_fields(shape, seed=5, n_gauss=4):
     }
 
 
+def laplace_neumann_fields(n):
+    """Cell-centred n x n Laplace problem with mirrored ghosts on all faces.
+
+    Restates ``srj/problems.py:246-276`` (laplace2d_neumann): h = 1/n, centre
+    4/h^2, neighbours -1/h^2, zero source; pair with MIRROR rules.
+    """
+    h = 1.0 / n
+    shape = (n, n)
+    off = -1.0 / h ** 2
+    return {"u": np.zeros((n + 2, n + 2)), "source": np.zeros(shape),
+            "center": np.full(shape, 4.0 / h ** 2), "lower": (np.full(shape, off),) * 2,
+            "upper": (np.full(shape, off),) * 2, "mask": None}
+
+
+GS_THETA = (0.3037, 2.8903)  # test-B arc ends on r = 1 (srj/problems.py:42-43)
+
+
+def grad_shafranov_fields(test, c, n):
+    """The paper's Grad-Shafranov benchmark (section 5.3) as fields.
+
+    Restates ``srj/problems.py:634-717``: Delta* psi + C^2 psi = 0 on
+    r in [1, 10] (n equispaced nodes incl. both ends, whose rows hold the
+    Dirichlet data) x theta in [0, pi] (n cells, cell centred, MIRROR ends).
+    Rows: center = -2/dr^2 - 2/(r^2 dth^2) + C^2; radial neighbours 1/dr^2;
+    theta neighbours (1/dth^2 -+ cot(theta)/(2 dth)) / r^2.  Test A: psi =
+    sin^2(theta)/r on r = 1 and r = 10.  Test B: sin^2 arc on r = 1 between
+    GS_THETA, zero elsewhere, relaxation restricted to the masked region
+    (shape curve minus the disk of radius 1 at (x, y) = (4, 1.6)).
+    Returns the field dict plus ``bc`` kinds ((fixed, fixed), (mirror, mirror)).
+    """
+    if test not in ("A", "B"):
+        raise ValueError("test must be 'A' or 'B'")
+    if n < 16:
+        raise ValueError("n must be at least 16")
+    dr = 9.0 / (n - 1)
+    dth = math.pi / n
+    r = 1.0 + np.arange(n) * dr
+    theta = 0.0 + (np.arange(n) + 0.5) * dth
+    ri = r[1:-1]
+    r2 = (ri ** 2)[:, None]
+    shape = (n - 2, n)
+    cot = 1.0 / np.tan(theta)
+    center = -2.0 / dr ** 2 - 2.0 / (r2 * dth ** 2) + c ** 2 + np.zeros(shape)
+    rad = np.full(shape, 1.0 / dr ** 2)
+    th_lo = (1.0 / dth ** 2 + cot[None, :] / (2.0 * dth)) / r2 + np.zeros(shape)
+    th_hi = (1.0 / dth ** 2 - cot[None, :] / (2.0 * dth)) / r2 + np.zeros(shape)
+    u = np.zeros((n, n + 2))
+    mask = None
+    if test == "A":
+        u[0, 1:-1] = np.sin(theta) ** 2 / r[0]
+        u[-1, 1:-1] = np.sin(theta) ** 2 / r[-1]
+    else:
+        t1, t2 = GS_THETA
+        arc = (theta >= t1) & (theta <= t2)
+        u[0, 1:-1] = np.where(arc, np.sin((theta - t1) / (t2 - t1) * math.pi) ** 2, 0.0)
+        rr, tt = ri[:, None], theta[None, :]
+        bound = (4.5 * np.sin(tt) ** 2 + 2.5 * np.sin(2.0 * tt) ** 2) * (
+            1.0 - 0.4 * np.cos(3.0 * tt) + 0.3 * np.cos(5.0 * tt) + 0.05 * np.sin(25.0 * tt))
+        x, y = rr * np.sin(tt), rr * np.cos(tt)
+        mask = (rr < bound) & ~((x - 4.0) ** 2 + (y - 1.6) ** 2 < 1.0)
+    return {"u": u, "source": np.zeros(shape), "center": center, "lower": (rad, th_lo),
+            "upper": (rad.copy(), th_hi), "mask": mask,
+            "bc": (("fixed", "fixed"), ("mirror", "mirror"))}
+
+
 def config_fields(name, shape=None):
     """Fields for a named BASELINE config, optionally at a reduced shape."""
     cfg = CONFIGS[name]

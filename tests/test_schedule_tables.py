@@ -95,3 +95,20 @@ def test_effective_n_matches_reference_examples():
     assert abs(effective_n((257, 257, 257), 3, "dirichlet") - 181.73) < 0.01
     assert config_schedule("cfg5").source_schedule.n == 150
     assert config_schedule("cfg2").m == 25530
+
+
+@pytest.mark.parametrize("test,c,n", [("A", 0.0, 40), ("A", 0.34, 33), ("B", 0.0, 48)])
+def test_grad_shafranov_builder_matches_reference(test, c, n):
+    """The restated paper benchmark problem equals srj.problems.grad_shafranov."""
+    from paper_1511_04292_b200.problems import grad_shafranov_fields
+
+    g = load_golden("builders")
+    tag = f"gs_{test}_{str(c).replace('.', 'p')}_{n}"
+    f = grad_shafranov_fields(test, c, n)
+    assert np.array_equal(f["u"], g[tag + "_u"])
+    assert np.array_equal(f["center"], g[tag + "_center"])
+    assert np.array_equal(f["lower"][0], g[tag + "_lower0"])
+    assert np.array_equal(f["lower"][1], g[tag + "_lower1"])
+    assert np.array_equal(f["upper"][1], g[tag + "_upper1"])
+    if test == "B":
+        assert np.array_equal(f["mask"], g[tag + "_mask"])
