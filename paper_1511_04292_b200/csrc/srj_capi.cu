@@ -18,6 +18,7 @@
 #include "srj_reduce.cuh"
 #include "srj_sweep2d.cuh"
 #include "srj_sweep3d.cuh"
+#include "srj_cluster2d.cuh"
 
 using namespace srj;
 
@@ -235,6 +236,10 @@ struct srj_plan {
   bool has_bc;       // some face is not FIXED: refresh ghosts after each sweep
   int default_fuse;
   double *partials;  // [kResidBlocks][2] device scratch
+  // small-grid cluster path: per-chunk omegas (device + pinned staging)
+  double *d_omegas = nullptr, *h_omegas = nullptr;
+  int64_t omega_cap = 0;
+  cudaEvent_t omega_ev = nullptr;
 };
 
 extern "C" {
@@ -366,6 +371,9 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
 int srj_plan_destroy(srj_plan *p) {
   if (!p) return SRJ_OK;
   if (p->partials) cudaFree(p->partials);
+  if (p->d_omegas) cudaFree(p->d_omegas);
+  if (p->h_omegas) cudaFreeHost(p->h_omegas);
+  if (p->omega_ev) cudaEventDestroy(p->omega_ev);
   delete p;
   return SRJ_OK;
 }
@@ -416,6 +424,137 @@ static int launch_ghosts(const srj_plan_desc &d, double *u0, cudaStream_t st) {
   return SRJ_OK;
 }
 
+}  // extern "C" (the small-grid helpers below are C++)
+
+// SRJ_SMALL=0 disables, =1 forces (when it fits) the cluster path; default:
+// used for whole-grid 2D plans of at most kSmallCells cells
+constexpr int64_t kSmallCells = 1 << 18;
+
+int small_mode() {
+  static int v = -2;
+  if (v == -2) {
+    const char *e = getenv("SRJ_SMALL");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+static bool cluster_fits(const srj_plan &plan, int &C, int &R) {
+  const srj_plan_desc &d = plan.d;
+  const srj_layout_t &l = d.layout;
+  if (l.ndim != 2 || !d.physical_lo0 || !d.physical_hi0 || l.halo0 != 1) return false;
+  if (d.own0_begin != 0 || d.own0_end != l.n[0]) return false;
+  const int mode = small_mode();
+  if (mode == 0) return false;
+  if (mode < 0 && l.n[0] * l.n[1] > kSmallCells) return false;
+  const int n0 = int(l.n[0]);
+  C = std::min(kClusterMax, n0);
+  R = (n0 + C - 1) / C;
+  C = (n0 + R - 1) / R;
+  if (R > kTY * kMaxA || l.n[1] > kTX * kMaxB) return false;  // register tiling limits
+  const size_t bytes = 2 * size_t(R + 2) * size_t(l.n[1] + 2) * 8;
+  return bytes <= 200 * 1024;
+}
+
+template <bool VAR, bool NL, bool RECIP>
+static int launch_cluster(const Cluster2DParams &p, int C, size_t smem, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(sweep2d_cluster<VAR, NL, RECIP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(sweep2d_cluster<VAR, NL, RECIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(kClusterThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SRJ_CUDA(cudaLaunchKernelEx(&cfg, sweep2d_cluster<VAR, NL, RECIP>, p));
+  return SRJ_OK;
+}
+
+static int run_cluster2d(srj_plan &plan, const double *src, double *dst, const double *weights,
+                         int64_t m, int64_t first, int64_t nsteps, double *d_norms,
+                         int32_t *final_buf, cudaStream_t st, int C, int R) {
+  const srj_plan_desc &d = plan.d;
+  const srj_layout_t &l = d.layout;
+  if (nsteps > plan.omega_cap) {
+    if (plan.d_omegas) cudaFree(plan.d_omegas);
+    if (plan.h_omegas) cudaFreeHost(plan.h_omegas);
+    plan.d_omegas = plan.h_omegas = nullptr;
+    plan.omega_cap = 0;
+    SRJ_CUDA(cudaMalloc(&plan.d_omegas, sizeof(double) * size_t(nsteps)));
+    SRJ_CUDA(cudaMallocHost(&plan.h_omegas, sizeof(double) * size_t(nsteps)));
+    if (!plan.omega_ev) SRJ_CUDA(cudaEventCreateWithFlags(&plan.omega_ev, cudaEventDisableTiming));
+    plan.omega_cap = nsteps;
+  } else if (plan.omega_ev) {
+    SRJ_CUDA(cudaEventSynchronize(plan.omega_ev));  // staging buffer free again
+  }
+  for (int64_t k = 0; k < nsteps; ++k) plan.h_omegas[k] = weights[(first + k) % m];
+  SRJ_CUDA(cudaMemcpyAsync(plan.d_omegas, plan.h_omegas, sizeof(double) * size_t(nsteps),
+                           cudaMemcpyHostToDevice, st));
+  SRJ_CUDA(cudaEventRecord(plan.omega_ev, st));
+  const int64_t ioff = interior_offset(l);
+  Cluster2DParams p{};
+  p.src = src + ioff;
+  p.dst = dst + ioff;
+  const bool nl = d.kappa != nullptr, var = d.coef_mode == 1;
+  p.f = (nl ? d.kappa : d.source) + ioff;
+  p.act = d.act ? d.act + ioff : nullptr;
+  if (var) {
+    p.c = d.coef_arrays[0] + ioff;
+    p.am0 = d.coef_arrays[1] + ioff;
+    p.ap0 = d.coef_arrays[2] + ioff;
+    p.am1 = d.coef_arrays[3] + ioff;
+    p.ap1 = d.coef_arrays[4] + ioff;
+  }
+  p.kc = d.coef[0];
+  p.kam0 = d.coef[1];
+  p.kap0 = d.coef[2];
+  p.kam1 = d.coef[3];
+  p.kap1 = d.coef[4];
+  p.pitch = l.pitch;
+  p.n0 = int(l.n[0]);
+  p.n1 = int(l.n[1]);
+  p.R = R;
+  p.sp = int(l.n[1]) + 2;
+  for (int a = 0; a < 2; ++a)
+    for (int side = 0; side < 2; ++side) {
+      p.bc_kind[a][side] = d.bc[a][side].kind;
+      p.bc_value[a][side] = d.bc[a][side].value;
+      p.bc_values[a][side] = d.bc[a][side].values;
+    }
+  p.omegas = plan.d_omegas;
+  p.nsteps = int(nsteps);
+  p.norms = d_norms;
+  const size_t smem = 2 * size_t(R + 2) * size_t(p.sp) * 8;
+  p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
+  const bool recip = !var && p.kinv != 0.0;
+  int rc;
+  if (var)
+    rc = nl ? launch_cluster<true, true, false>(p, C, smem, st)
+            : launch_cluster<true, false, false>(p, C, smem, st);
+  else if (recip)
+    rc = nl ? launch_cluster<false, true, true>(p, C, smem, st)
+            : launch_cluster<false, false, true>(p, C, smem, st);
+  else
+    rc = nl ? launch_cluster<false, true, false>(p, C, smem, st)
+            : launch_cluster<false, false, false>(p, C, smem, st);
+  if (rc != SRJ_OK) return rc;
+  *final_buf = 1;
+  return SRJ_OK;
+}
+
+extern "C" {
+
 int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b,
                  const double *weights, int64_t m, int64_t first, int64_t nsteps, int32_t fuse,
                  double *d_norms, int32_t *final_buf, void *stream) {
@@ -446,6 +585,10 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
   row_ranges(d, lo_c, hi_c, ld_lo, ld_hi);
   const int rows = int(d.own0_end - d.own0_begin);
 
+  if (l.ndim == 2) {
+    int C = 0, R = 0;
+    if (cluster_fits(*plan, C, R)) return run_cluster2d(*plan, src, buf_a, weights, m, first, nsteps, d_norms, final_buf, st, C, R);
+  }
   const double *cur = src;
   double *nxt = buf_a;
   int which = 1;

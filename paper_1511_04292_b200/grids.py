@@ -333,12 +333,20 @@ def _solve(problem, weights, tol, max_iters, normalise, stop, check_every, fuse,
                 l2_reference = float(np.sqrt(np.sum(np.square(problem.source))))
         if l2_reference == 0.0:
             l2_reference = 1.0
-        span = every
+        span = cap = every
+    elif chunk:
+        span = cap = int(chunk)
     else:
-        span = int(chunk) if chunk else int(min(65536, max(64, 0.1 / _step_seconds_estimate(problem))))
+        # host checks of the per-step norms: the first chunk covers ~2 ms of
+        # work, each next one doubles up to ~50 ms, so replaying the chunk in
+        # which the rule fires costs at most about as much as the work so far
+        est = _step_seconds_estimate(problem)
+        cap = int(min(65536, max(64, 0.05 / est)))
+        span = int(min(cap, max(32, 0.002 / est)))
     try:
         while done < max_iters:
             n = min(span, max_iters - done)
+            span = min(cap, 2 * span)
             if stop == "residual_l2":
                 n = min(n, every - done % every)
             out = dev.run(cur, w, done, n, fuse)

@@ -383,3 +383,20 @@ def test_masked_cells_never_written():
     run_steps(p, np.ones(1), 150)
     assert np.array_equal(p.interior[inert], before)
     assert np.any(p.interior[p.mask] != 0.0)
+
+
+def test_band_kernels_without_cluster_path():
+    """Small fixtures normally take the DSMEM cluster kernel; re-run the parity
+    suite with it disabled so the fused band kernels are checked at small
+    sizes too (SRJ_SMALL is read once per process, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SRJ_SMALL="0")
+    here = os.path.dirname(os.path.abspath(__file__))
+    res = subprocess.run(
+        [sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", os.path.join(here, "test_gpu_parity.py"),
+         "-k", "not band_kernels_without and not reciprocal"],
+        env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
