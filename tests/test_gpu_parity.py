@@ -400,3 +400,79 @@ def test_band_kernels_without_cluster_path():
          "-k", "not band_kernels_without and not reciprocal"],
         env=env, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+
+
+# --------------------------------------------- paper claims on the GPU path
+def _neumann(n):
+    from paper_1511_04292_b200.problems import laplace_neumann_fields
+
+    f = laplace_neumann_fields(n)
+    return G.GridProblem(spacing=(1.0 / n,) * 2, u=f["u"], source=f["source"],
+                         center=f["center"], lower=f["lower"], upper=f["upper"],
+                         bc=((G.MIRROR, G.MIRROR),) * 2)
+
+
+def _smooth_init(p, seed=0):
+    """Slow cosine modes (test_grids.py:47-66 fixture, restated)."""
+    n = p.shape[0]
+    xc = (np.arange(n) + 0.5) / n
+    rng = np.random.default_rng(seed)
+    u = np.zeros(p.shape)
+    for k in range(4):
+        for m in range(4):
+            a = rng.standard_normal()
+            if k == 0 and m == 0:
+                continue
+            u += a * np.outer(np.cos(k * np.pi * xc), np.cos(m * np.pi * xc))
+    p.interior[...] = u
+    p.refresh_ghosts()
+    return p
+
+
+def test_measured_speedup_tracks_rho(table):
+    # test_grids.py:347-356: Laplace N=64 Neumann, P=6, ratio within 25% of rho
+    jac, _ = G.jacobi_solve(_smooth_init(_neumann(64)), 1e-10)
+    row = table.get(6, 64)
+    srj, _ = G.srj_solve(_smooth_init(_neumann(64)), quantize(row), 1e-10)
+    assert jac.converged and srj.converged
+    assert jac.iterations / srj.iterations == pytest.approx(row.rho, rel=0.25)
+
+
+def test_jacobi_iterations_scale_with_grid_area():
+    # test_grids.py:358-365
+    counts = {n: G.jacobi_solve(_smooth_init(_neumann(n)), 1e-10)[0].iterations
+              for n in (32, 64)}
+    assert 3.4 <= counts[64] / counts[32] <= 4.6
+
+
+def test_residual_drops_every_cycle(table):
+    # test_grids.py:390-404: every shipped P at N=64 contracts over each M-cycle
+    sizes = sorted(p for p, n in table.keys() if n == 64)
+    assert len(sizes) >= 10
+    rng = np.random.default_rng(7)
+    for p_levels in sizes:
+        cyc = quantize(table.get(p_levels, 64))
+        prob = _neumann(64)
+        prob.interior[...] = rng.standard_normal(prob.shape)
+        prob.refresh_ghosts()
+        hist, _ = G.srj_solve(prob, cyc, tol=1e-300, max_iters=2 * cyc.m + 1)
+        r = hist.true_residual_inf
+        assert r[cyc.m] < r[0], f"P={p_levels}: first cycle did not contract"
+        assert r[2 * cyc.m] < r[cyc.m], f"P={p_levels}: second cycle stalled"
+
+
+def test_cycle_permutation_changes_nothing_after_full_cycles(table):
+    # test_grids.py:406-419
+    cyc = quantize(table.get(6, 32))
+    rolled = np.roll(cyc.weight_sequence, 7)
+    steps = 3 * cyc.m
+    rng = np.random.default_rng(11)
+    init = rng.standard_normal((32, 32))
+    a, b = _neumann(32), _neumann(32)
+    for p in (a, b):
+        p.interior[...] = init
+        p.refresh_ghosts()
+    G.srj_solve(a, cyc, tol=1e-300, max_iters=steps)
+    G.srj_solve(b, Cycle(rolled), tol=1e-300, max_iters=steps)
+    scale = max(1.0, np.max(np.abs(a.interior)))
+    assert np.max(np.abs(a.interior - b.interior)) <= 1e-8 * scale
