@@ -19,6 +19,7 @@
 #include "srj_sweep2d.cuh"
 #include "srj_sweep3d.cuh"
 #include "srj_cluster2d.cuh"
+#include "srj_sweep3d_tb.cuh"
 
 using namespace srj;
 
@@ -166,6 +167,59 @@ struct K3 {
   static Kernel3D get() { return Kernel3D{launch, bps}; }
 };
 
+// temporally blocked 3D (constant stencil only)
+constexpr int kMaxFuse3D = 2;  // T=3 traps (under investigation), T=4 exceeds smem
+
+struct Kernel3DTB {
+  void (*launch)(const Sweep3DTBParams &, const CUtensorMap &, const CUtensorMap &, int,
+                 cudaStream_t);
+  int (*blocks_per_sm)();
+  int tj, tk, box_cols, box_rows;
+};
+
+template <int T, bool NL, bool RECIP>
+struct K3TB {
+  using B = Tile3D<T>;
+  static void configure() {
+    static bool done = false;
+    if (!done) {
+      cudaFuncSetAttribute(sweep3d_tb<T, NL, RECIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(B::smem_bytes()));
+      done = true;
+    }
+  }
+  static void launch(const Sweep3DTBParams &p, const CUtensorMap &tu, const CUtensorMap &tf,
+                     int blocks, cudaStream_t s) {
+    configure();
+    sweep3d_tb<T, NL, RECIP><<<blocks, B::THREADS, B::smem_bytes(), s>>>(p, tu, tf);
+  }
+  static int bps() {
+    static int n = 0;
+    if (n == 0) {
+      configure();
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d_tb<T, NL, RECIP>, B::THREADS,
+                                                    B::smem_bytes());
+      if (n <= 0) n = 1;
+    }
+    return n;
+  }
+  static Kernel3DTB get() { return Kernel3DTB{launch, bps, B::TJ, B::TK, B::HK, B::HJ}; }
+};
+
+template <int T>
+Kernel3DTB pick3d_tb_t(bool nl, bool recip) {
+  if (recip) return nl ? K3TB<T, true, true>::get() : K3TB<T, false, true>::get();
+  return nl ? K3TB<T, true, false>::get() : K3TB<T, false, false>::get();
+}
+
+Kernel3DTB pick3d_tb(int T, bool nl, bool recip) {
+  switch (T) {
+    case 2: return pick3d_tb_t<2>(nl, recip);
+    case 3: return pick3d_tb_t<3>(nl, recip);
+    default: return pick3d_tb_t<4>(nl, recip);
+  }
+}
+
 Kernel3D pick3d(bool var, bool nl, bool recip) {
   if (var) return nl ? K3<true, true, false>::get() : K3<true, false, false>::get();
   if (recip) return nl ? K3<false, true, true>::get() : K3<false, false, true>::get();
@@ -188,12 +242,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2D tensor map over a whole padded 2D field: rows0 rows of `pitch` doubles,
 // box = box_cols x 3 rows (one TMA group of the band kernel).
-int make_tmap(CUtensorMap *m, const double *base, const srj_layout_t &l, int box_cols) {
+int make_tmap(CUtensorMap *m, const double *base, const srj_layout_t &l, int box_cols,
+              int box_rows = 3) {
   auto fn = encode_fn();
   if (!fn) return fail(SRJ_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[2] = {cuuint64_t(l.pitch), cuuint64_t(l.rows0)};
+  // every last-axis row of the field is one tensor row (3D: planes x rows)
+  const int64_t rows = l.ndim == 3 ? l.rows0 * (l.n[1] + 2) : l.rows0;
+  cuuint64_t dims[2] = {cuuint64_t(l.pitch), cuuint64_t(rows)};
   cuuint64_t strides[1] = {cuuint64_t(l.pitch) * 8};
-  cuuint32_t box[2] = {cuuint32_t(box_cols), 3};
+  cuuint32_t box[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -357,7 +414,7 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
     return fail(SRJ_EUNSUPPORTED, "non-FIXED boundary rules need the whole grid on one plan");
   }
   // non-FIXED ghosts change every step: one sweep per launch + refresh
-  p->default_fuse = (l.ndim == 2 && desc->coef_mode == 0 && !p->has_bc) ? 4 : 1;
+  p->default_fuse = (desc->coef_mode == 0 && !p->has_bc) ? (l.ndim == 2 ? 4 : 2) : 1;
   p->partials = nullptr;
   cudaError_t e = cudaMalloc(&p->partials, sizeof(double) * 2 * kResidBlocks);
   if (e != cudaSuccess) {
@@ -571,7 +628,8 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
   const srj_layout_t &l = d.layout;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int T = fuse > 0 ? fuse : plan->default_fuse;
-  if (l.ndim == 3 || plan->has_bc) T = 1;
+  if (plan->has_bc || (l.ndim == 3 && d.coef_mode == 1)) T = 1;
+  if (l.ndim == 3 && T > kMaxFuse3D) T = kMaxFuse3D;
   if (T > kMaxFuse) return fail(SRJ_EINVAL, "fuse depth %d exceeds %d", T, kMaxFuse);
   if ((!d.physical_lo0 || !d.physical_hi0) && T > l.halo0)
     return fail(SRJ_EINVAL, "fuse depth %d needs halo0 >= %d on exchanged faces", T, T);
@@ -645,6 +703,51 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       const int warps = p.nbands * p.nstrips;
       const int blocks = (warps + Band2D<1, 2>::WARPS - 1) / Band2D<1, 2>::WARPS;
       k2.launch(p, tu, tf, blocks, st);
+    } else if (t > 1) {
+      // temporally blocked 3D (constant stencil): t fused sweeps per launch
+      Sweep3DTBParams p{};
+      p.dst = nxt + ioff;
+      for (int a = 0; a < 7; ++a) p.kc[a] = d.coef[a];
+      p.kinv = recip_or_zero(d.coef[0]);
+      p.pitch = l.pitch;
+      p.plane = l.plane;
+      p.n0 = int(l.n[0]);
+      p.n1 = int(l.n[1]);
+      p.n2 = int(l.n[2]);
+      p.ld_lo = ld_lo;
+      p.ld_hi = ld_hi;
+      p.own_b = int(d.own0_begin);
+      p.own_e = int(d.own0_end);
+      p.tma_col0 = int(l.origin + 1);
+      p.rows_per_plane = int(l.n[1] + 2);
+      p.tma_row0 = l.halo0 * p.rows_per_plane + 1;  // row of (i=0, j=0)
+      for (int q = 0; q < t; ++q) p.omega[q] = weights[(first + k + q) % m];
+      p.norms = d_norms + 2 * k;
+      const Kernel3DTB k3 = pick3d_tb(t, nl, p.kinv != 0.0);
+      p.ntj = int((l.n[1] + k3.tj - 1) / k3.tj);
+      p.ntk = int((l.n[2] + k3.tk - 1) / k3.tk);
+      const long tiles = long(p.ntj) * p.ntk;
+      const long capacity = long(sm_count()) * k3.blocks_per_sm();
+      int nstrips = 1;
+      double best = -1.0;
+      for (int ns = 1; ns <= std::max(1, std::min(64, rows / (4 * t))); ++ns) {
+        const long w = tiles * ns;
+        const long waves = (w + capacity - 1) / capacity;
+        const double hh = double(rows) / ns;
+        const double eff = double(w) / double(waves * capacity) * hh / (hh + 2.0 * t);
+        if (eff > best + 1e-9) {
+          best = eff;
+          nstrips = ns;
+        }
+      }
+      p.H = (rows + nstrips - 1) / nstrips;
+      p.nstrips = (rows + p.H - 1) / p.H;
+      CUtensorMap tu, tf;
+      int rc = make_tmap(&tu, cur, l, k3.box_cols, k3.box_rows);
+      if (rc != SRJ_OK) return rc;
+      rc = make_tmap(&tf, f, l, k3.box_cols, k3.box_rows);
+      if (rc != SRJ_OK) return rc;
+      k3.launch(p, tu, tf, int(tiles * p.nstrips), st);
     } else {
       Sweep3DParams p{};
       p.src = cur + ioff;

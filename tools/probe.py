@@ -65,13 +65,15 @@ def main():
     for n in [int(x) for x in a.three.split(",") if x]:
         f3 = config_fields("cfg3", (n, n, n))
         w3 = quantize(tab.lookup(10, 512)).weight_sequence
-        ms, g, frac = measure(f3, w3, 40, 1)
-        print(json.dumps(dict(kind="3d", n=n, ms_per_sweep=ms, glups=g, frac_alg=frac)), flush=True)
+        for fuse3 in (1, 2):
+            ms, g, frac = measure(f3, w3, 48, fuse3)
+            print(json.dumps(dict(kind="3d", n=n, fuse=fuse3, ms_per_sweep=ms, glups=g,
+                                  frac_alg=frac)), flush=True)
     if not a.nl:
         return
     f5 = config_fields("cfg5", (256, 256, 256))
     w5 = quantize(tab.lookup(8, 256)).weight_sequence
-    ms, g, frac = measure(f5, w5, 40, 1)
+    ms, g, frac = measure(f5, w5, 48, 0)
     print(json.dumps(dict(kind="3d-nl", n=256, ms_per_sweep=ms, glups=g, frac_alg=frac)), flush=True)
 
 
