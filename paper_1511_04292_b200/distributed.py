@@ -184,6 +184,8 @@ class DeviceSlab:
         self.plane = int(self.grid.layout.plane)
         self.origin = int(self.grid.layout.origin)
         self.stream = self.grid.stream
+        # deepest single-launch fusion the plan runs (libsrj srj_plan_run)
+        self.max_fuse = (4 if self.grid.ndim == 2 else 2) if self.grid.constant else 1
 
     def reserve(self, nsteps):
         self.grid.ensure_norms(nsteps)
@@ -239,7 +241,8 @@ class SlabGrid:
         n0 = fields["source"].shape[0]
         self.decomp = SlabDecomposition(n0, world, rank, halo=max(1, fuse))
         self.backend = DeviceSlab(fields, self.decomp)
-        self.solver = SlabSolver(self.backend, self.decomp, group=group, fuse=max(1, fuse))
+        fuse = max(1, min(fuse, self.backend.max_fuse))
+        self.solver = SlabSolver(self.backend, self.decomp, group=group, fuse=fuse)
         self.stream = self.backend.stream
         self._norms = None
         self.torch = torch

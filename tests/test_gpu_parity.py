@@ -329,12 +329,13 @@ def test_slab_decomposition_bitwise_on_one_gpu(table, world, fuse):
     assert np.array_equal(norms[:, 1], hist.true_residual_inf)
 
 
-def test_slab_decomposition_3d_on_one_gpu(table):
+@pytest.mark.parametrize("fuse", [1, 2])
+def test_slab_decomposition_3d_on_one_gpu(table, fuse):
     f = config_fields("cfg3", (37, 30, 66))
     w = quantize(table.lookup(10, 512)).weight_sequence
-    field, norms = _EmulatedRanks(f, 3, 1).run(w, 40)
+    field, norms = _EmulatedRanks(f, 3, fuse).run(w, 40)
     p = problem_from(f)
-    hist, _ = run_steps(p, w, 40)
+    hist, _ = run_steps(p, w, 40, fuse=1)
     assert np.array_equal(field, p.interior)
     assert np.array_equal(norms[:, 1], hist.true_residual_inf)
 
