@@ -477,3 +477,42 @@ def test_cycle_permutation_changes_nothing_after_full_cycles(table):
     G.srj_solve(b, Cycle(rolled), tol=1e-300, max_iters=steps)
     scale = max(1.0, np.max(np.abs(a.interior)))
     assert np.max(np.abs(a.interior - b.interior)) <= 1e-8 * scale
+
+
+# ------------------------------------------------------------ edge shapes
+EDGE_2D = [(1, 1), (1, 7), (3, 5), (2, 64), (5, 63), (7, 65), (9, 130), (33, 1), (64, 2),
+           (13, 200)]
+EDGE_3D = [(1, 1, 1), (2, 3, 4), (3, 1, 70), (5, 17, 1), (9, 20, 65), (18, 3, 129)]
+
+
+@pytest.mark.parametrize("shape", EDGE_2D + EDGE_3D)
+@pytest.mark.parametrize("fuse", [1, 4])
+def test_edge_shapes_bitwise(table, shape, fuse):
+    """Tiny, ragged and sub-band grids through every kernel path (the cluster
+    path by default; the band/tile kernels in the SRJ_SMALL=0 rerun)."""
+    rng = np.random.default_rng(len(shape) * 100 + sum(shape))
+    f = config_fields("cfg2", shape) if len(shape) == 2 else config_fields("cfg3", shape)
+    f["u"] = rng.standard_normal(f["u"].shape)
+    w = quantize(table.get(6, 64)).weight_sequence
+    want, norms = oracle_steps(f, w, 60)
+    p = problem_from(f)
+    hist, _ = run_steps(p, w, 60, fuse=fuse, chunk=23)
+    assert np.array_equal(p.u, want.u)
+    assert np.array_equal(hist.true_residual_inf, norms[:, 1])
+
+
+@pytest.mark.parametrize("shape", [(6, 9), (4, 5, 6)])
+def test_edge_shapes_variable_and_masked(shape):
+    rng = np.random.default_rng(5)
+    nd = len(shape)
+    f = {"u": rng.standard_normal(tuple(s + 2 for s in shape)),
+         "source": rng.standard_normal(shape), "center": rng.uniform(4, 8, shape),
+         "lower": tuple(-rng.uniform(0.5, 1, shape) for _ in range(nd)),
+         "upper": tuple(-rng.uniform(0.5, 1, shape) for _ in range(nd)),
+         "mask": rng.uniform(size=shape) > 0.3}
+    w = np.array([3.0, 0.5, 1.7, 0.9])
+    want, norms = oracle_steps(f, w, 40)
+    p = problem_from(f)
+    hist, _ = run_steps(p, w, 40, chunk=9)
+    assert np.array_equal(p.u, want.u)
+    assert np.array_equal(hist.true_residual_inf, norms[:, 1])
