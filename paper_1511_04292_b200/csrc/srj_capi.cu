@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -54,6 +55,13 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // y = RN(1/c) for the reciprocal division path (srj_sweep2d.cuh div_by_const),
 // or 0 to keep the IEEE division when c is outside [2^-100, 2^100].
+// low word of the double-word reciprocal: yl = RN(1/c - yh), via the exact
+// FMA remainder 1 - c*yh
+double recip_lo(double c, double yh) {
+  if (yh == 0.0) return 0.0;
+  return std::fma(-c, yh, 1.0) / c;
+}
+
 double recip_or_zero(double c) {
   if (!(c >= 0x1p-100 && c <= 0x1p+100)) return 0.0;  // c > 0 only (div_recip sign rule)
   return 1.0 / c;
@@ -274,13 +282,13 @@ Kernel2D pick2d(int T, bool var, bool nl, bool recip) {
 
 }  // namespace
 
-__global__ void selftest_div(const double *a, int64_t n, double c, double y, double *out,
-                             double *ref) {
+__global__ void selftest_div(const double *a, int64_t n, double c, double y, double yl,
+                             double *out, double *ref) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     double q = __ddiv_rn(a[i], c);
     if (y != 0.0) {  // exactly what the RECIP sweep kernels compute
-      q = div_recip(a[i], c, y);
+      q = div_recip(a[i], c, y, yl);
       if (recip_unsafe(a[i])) q = div_ieee(a[i], c);
     }
     out[i] = q;
@@ -308,8 +316,9 @@ int srj_selftest_div(const double *a, int64_t n, double c, double *out, double *
   if (!a || !out || !ref || n < 0) return fail(SRJ_EINVAL, "bad argument");
   if (n == 0) return SRJ_OK;
   const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(sm_count()) * 32));
-  selftest_div<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, n, c, recip_or_zero(c),
-                                                                       out, ref);
+  const double yh = recip_or_zero(c);
+  selftest_div<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, n, c, yh,
+                                                                       recip_lo(c, yh), out, ref);
   SRJ_CUDA(cudaGetLastError());
   return SRJ_OK;
 }
@@ -594,6 +603,7 @@ static int run_cluster2d(srj_plan &plan, const double *src, double *dst, const d
   p.norms = d_norms;
   const size_t smem = 2 * size_t(R + 2) * size_t(p.sp) * 8;
   p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
+  p.kinv_lo = recip_lo(d.coef[0], p.kinv);
   const bool recip = !var && p.kinv != 0.0;
   int rc;
   if (var)
@@ -672,6 +682,7 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.kam1 = d.coef[3];
       p.kap1 = d.coef[4];
       p.kinv = recip_or_zero(d.coef[0]);
+      p.kinv_lo = recip_lo(d.coef[0], p.kinv);
       p.pitch = l.pitch;
       p.n0 = int(l.n[0]);
       p.n1 = int(l.n[1]);
@@ -709,6 +720,7 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.dst = nxt + ioff;
       for (int a = 0; a < 7; ++a) p.kc[a] = d.coef[a];
       p.kinv = recip_or_zero(d.coef[0]);
+      p.kinv_lo = recip_lo(d.coef[0], p.kinv);
       p.pitch = l.pitch;
       p.plane = l.plane;
       p.n0 = int(l.n[0]);
@@ -773,6 +785,7 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.nbands = int((l.n[2] + 63) / 64);
       p.njg = int((l.n[1] + kRows3D - 1) / kRows3D);
       p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
+      p.kinv_lo = recip_lo(d.coef[0], p.kinv);
       const bool recip = !var && p.kinv != 0.0;
       const Kernel3D k3 = pick3d(var, nl, recip);
       const long per_strip = long(p.njg) * p.nbands;

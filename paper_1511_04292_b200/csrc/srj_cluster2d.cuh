@@ -41,6 +41,7 @@ struct Cluster2DParams {
   const double *c, *am0, *ap0, *am1, *ap1;  // VAR coefficients (padded layout)
   double kc, kam0, kap0, kam1, kap1;
   double kinv;             // RN(1/kc) for the reciprocal division (RECIP)
+  double kinv_lo;      // RN(1/c - kinv): low word of the reciprocal
   int64_t pitch;           // global row pitch (elements)
   int n0, n1;
   int R;                   // rows per CTA
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
         const double nm = __dmul_rn(om, rr);
         double d;
         if (RECIP && !ieee) {
-          d = div_recip(nm, p.kc, p.kinv);
+          d = div_recip(nm, p.kc, p.kinv, p.kinv_lo);
           bad |= recip_unsafe(nm);
         } else {
           d = (RECIP ? div_ieee(nm, c) : __ddiv_rn(nm, c));

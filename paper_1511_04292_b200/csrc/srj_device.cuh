@@ -80,21 +80,19 @@ __device__ __forceinline__ void global_max(double *slot, double v) {
               static_cast<unsigned long long>(__double_as_longlong(v)));
 }
 
-// RN(a/c) for a fixed divisor c > 0 with y = RN(1/c), branch-free:
-// q0 = RN(a*y) is within 1.5 ulp of a/c; one Markstein correction
-// q1 = RN(q0 + RN(a - c*q0)*y) brings it within 1 ulp; with q1 faithful and y
-// within 1/2 ulp of 1/c, Markstein's theorem makes r1 = a - c*q1 exact and
-// RN(q1 + r1*y) = RN(a/c).  The sign is copied from a, which is exact for
+// RN(a/c) for a fixed divisor c > 0 from a double-word reciprocal
+// (yh = RN(1/c), yl = RN(1/c - yh), host-computed), branch-free, 4 FP64 ops.  The sign is copied from a, which is exact for
 // c > 0 and restores IEEE's -0/c = -0.  Valid for a = +-0 and for normal a
 // with exponent in [-899, 899] (no overflow/underflow in q, r); other inputs
 // (subnormal, huge, inf, NaN) are flagged by recip_unsafe() and redone with
 // the IEEE division after a warp vote (see stage2d).
-__device__ __forceinline__ double div_recip(double a, double c, double y) {
-  double q = __dmul_rn(a, y);
-  double r = __fma_rn(-q, c, a);
-  q = __fma_rn(r, y, q);
-  r = __fma_rn(-q, c, a);
-  q = __fma_rn(r, y, q);
+__device__ __forceinline__ double div_recip(double a, double c, double yh, double yl) {
+  // q0 = RN(a*yh + RN(a*yl)) with yh + yl = 1/c to ~2^-106 is faithful (within
+  // 1 ulp of a/c); Markstein's theorem (yh within 1/2 ulp of 1/c, q0 faithful)
+  // then makes the remainder exact and one correction correctly rounded.
+  double q = __fma_rn(a, yh, __dmul_rn(a, yl));
+  const double r = __fma_rn(-q, c, a);
+  q = __fma_rn(r, yh, q);
   const int hi = (__double2hiint(q) & 0x7fffffff) | (__double2hiint(a) & int(0x80000000));
   return __hiloint2double(hi, __double2loint(q));
 }

@@ -47,6 +47,7 @@ struct Sweep2DParams {
   const double *c, *am0, *ap0, *am1, *ap1;  // per-cell coefficients (VAR)
   double kc, kam0, kap0, kam1, kap1;        // constant stencil (!VAR)
   double kinv;         // RN(1/kc) when the reciprocal division is safe, else 0
+  double kinv_lo;      // RN(1/c - kinv): low word of the reciprocal
   int64_t pitch;       // elements per row
   int n0, n1;          // interior extents
   int lo_c, hi_c;      // rows that relax (others pass through): [lo_c, hi_c)
@@ -147,7 +148,7 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, const double (&u
     const double uc = mid[v];
     double d;
     if (RECIP) {
-      d = div_recip(num[v], p.kc, p.kinv);
+      d = div_recip(num[v], p.kc, p.kinv, p.kinv_lo);
       bad |= recip_unsafe(num[v]);
     } else {
       d = __ddiv_rn(num[v], cv[v]);

@@ -23,6 +23,7 @@ struct Sweep3DParams {
   const double *coef[7];  // c, am0, ap0, am1, ap1, am2, ap2 (VAR)
   double kc[7];           // constant stencil
   double kinv;            // RN(1/kc[0]) when the reciprocal path is used
+  double kinv_lo;      // RN(1/c - kinv): low word of the reciprocal
   int64_t pitch, plane;
   int n0, n1, n2;
   int lo_c, hi_c, ld_lo, ld_hi, own_b, own_e;
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kWarps3D * 32)
           if (!act) nm = 1.0;  // keep garbage off the IEEE fixup path
           double d;
           if (RECIP) {
-            d = div_recip(nm, p.kc[0], p.kinv);
+            d = div_recip(nm, p.kc[0], p.kinv, p.kinv_lo);
             bad |= recip_unsafe(nm);
           } else {
             d = __ddiv_rn(nm, k[0]);

@@ -22,6 +22,7 @@ struct Sweep3DTBParams {
   double *dst;         // interior origin of the output
   double kc[7];        // constant stencil
   double kinv;         // RN(1/kc[0]) or 0 (IEEE division)
+  double kinv_lo;      // RN(1/c - kinv): low word of the reciprocal
   int64_t pitch, plane;
   int n0, n1, n2;
   int ld_lo, ld_hi;    // planes present (interior indices)
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, 1)
             num[u] = __dmul_rn(om, rr);
             double d;
             if (RECIP) {
-              d = div_recip(num[u], p.kc[0], p.kinv);
+              d = div_recip(num[u], p.kc[0], p.kinv, p.kinv_lo);
               bad |= recip_unsafe(num[u]);
             } else {
               d = __ddiv_rn(num[u], p.kc[0]);
