@@ -176,7 +176,7 @@ struct K3 {
 };
 
 // temporally blocked 3D (constant stencil only)
-constexpr int kMaxFuse3D = 2;  // T=3 traps (under investigation), T=4 exceeds smem
+constexpr int kMaxFuse3D = 3;  // T=4 tiles exceed shared memory
 
 struct Kernel3DTB {
   void (*launch)(const Sweep3DTBParams &, const CUtensorMap &, const CUtensorMap &, int,
@@ -211,7 +211,7 @@ struct K3TB {
     }
     return n;
   }
-  static Kernel3DTB get() { return Kernel3DTB{launch, bps, B::TJ, B::TK, B::HK, B::HJ}; }
+  static Kernel3DTB get() { return Kernel3DTB{launch, bps, B::TJ, B::TK, B::HS, B::HJ}; }
 };
 
 template <int T>

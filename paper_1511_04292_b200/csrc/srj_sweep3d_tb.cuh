@@ -39,12 +39,18 @@ template <int T>
 struct Tile3D {
   static constexpr int TJ = 16, TK = 64;                 // owned cells per tile
   static constexpr int HJ = TJ + 2 * T, HK = TK + 2 * T; // loaded tile
+  // A TMA box must start on a 16-B aligned column (an fp64 box at an odd
+  // column faults): for odd T the box starts one column left of the tile
+  // (KOFF) and is widened to an even number of columns (HS, the smem row
+  // stride).  Tile cell (jj, kk) lives at jj * HS + kk + KOFF.
+  static constexpr int KOFF = T & 1;
+  static constexpr int HS = (HK + KOFF + 1) / 2 * 2;
   static constexpr int L = (T > 2 ? T : 2);              // ticks a slot stays live
   static constexpr int NS = L + 3;                       // slots: prefetch 2 planes
   static constexpr int THREADS = 512;
-  static constexpr int BOX_BYTES = HJ * HK * 8;          // one TMA box (u or f)
+  static constexpr int BOX_BYTES = HJ * HS * 8;          // one TMA box (u or f)
   // slot stride padded to 128 B: every TMA destination must be 128-B aligned
-  static constexpr int TILE = (HJ * HK + 15) / 16 * 16;  // doubles per slot
+  static constexpr int TILE = (HJ * HS + 15) / 16 * 16;  // doubles per slot
   static constexpr size_t smem_bytes() {
     // NS x (u + f) tiles, (T-1) stage windows of 3 planes, NS barriers
     return size_t(NS) * 2 * TILE * 8 + size_t(T > 1 ? T - 1 : 0) * 3 * TILE * 8 +
@@ -58,6 +64,7 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, 1)
                const __grid_constant__ CUtensorMap tm_f) {
   using B = Tile3D<T>;
   constexpr int HJ = B::HJ, HK = B::HK, TJ = B::TJ, TK = B::TK, NS = B::NS, TILE = B::TILE;
+  constexpr int HS = B::HS, KOFF = B::KOFF;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   double *ring_u = reinterpret_cast<double *>(smem_raw);  // NS tiles
   double *ring_f = ring_u + NS * TILE;                    // NS tiles
@@ -83,13 +90,13 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, 1)
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
         "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_addr(ring_u + s * TILE)),
-        "l"(reinterpret_cast<uint64_t>(&tm_u)), "r"(p.tma_col0 + k0), "r"(row),
+        "l"(reinterpret_cast<uint64_t>(&tm_u)), "r"(p.tma_col0 + k0 - KOFF), "r"(row),
         "r"(smem_addr(&bars[s]))
         : "memory");
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
         "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_addr(ring_f + s * TILE)),
-        "l"(reinterpret_cast<uint64_t>(&tm_f)), "r"(p.tma_col0 + k0), "r"(row),
+        "l"(reinterpret_cast<uint64_t>(&tm_f)), "r"(p.tma_col0 + k0 - KOFF), "r"(row),
         "r"(smem_addr(&bars[s]))
         : "memory");
   };
@@ -146,7 +153,7 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, 1)
           const int q = tid + (itr * U + u) * B::THREADS;
           const bool in = q < NCELL;
           const int jj = t + (in ? q : 0) / RK, kk = t + (in ? q : 0) % RK;
-          o[u] = jj * HK + kk;
+          o[u] = jj * HS + kk + KOFF;
           const int j = j0 + jj, k = k0 + kk;
           uc[u] = md[o[u]];
           act[u] = in && plane_act && j >= 0 && j < p.n1 && k >= 0 && k < p.n2;
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, 1)
           if (act[u]) {
             const double sv = NL ? nl_source(fp[o[u]], uc[u]) : fp[o[u]];
             const double rr = resid7(sv, p.kc[0], uc[u], p.kc[1], up[o[u]], p.kc[2], dn[o[u]],
-                                     p.kc[3], md[o[u] - HK], p.kc[4], md[o[u] + HK], p.kc[5],
+                                     p.kc[3], md[o[u] - HS], p.kc[4], md[o[u] + HS], p.kc[5],
                                      md[o[u] - 1], p.kc[6], md[o[u] + 1]);
             num[u] = __dmul_rn(om, rr);
             double d;
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, 1)
           if (t < T) {
             out[o[u]] = y[u];
           } else if (own[u]) {
-            const int jj = o[u] / HK, kk = o[u] % HK;
+            const int jj = (o[u] - KOFF) / HS, kk = (o[u] - KOFF) % HS;
             p.dst[int64_t(pl) * p.plane + int64_t(j0 + jj) * p.pitch + (k0 + kk)] = y[u];
           }
         }

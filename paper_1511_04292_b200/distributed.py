@@ -185,7 +185,7 @@ class DeviceSlab:
         self.origin = int(self.grid.layout.origin)
         self.stream = self.grid.stream
         # deepest single-launch fusion the plan runs (libsrj srj_plan_run)
-        self.max_fuse = (4 if self.grid.ndim == 2 else 2) if self.grid.constant else 1
+        self.max_fuse = (4 if self.grid.ndim == 2 else 3) if self.grid.constant else 1
 
     def reserve(self, nsteps):
         self.grid.ensure_norms(nsteps)

@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_1511_04292_b200.engine import DeviceGrid  # noqa: E402
-from paper_1511_04292_b200.problems import config_fields  # noqa: E402
+from paper_1511_04292_b200.problems import config_fields, config_schedule  # noqa: E402
 from paper_1511_04292_b200.schedule import quantize  # noqa: E402
 from paper_1511_04292_b200.tables import shipped_table  # noqa: E402
 
@@ -65,14 +65,14 @@ def main():
     for n in [int(x) for x in a.three.split(",") if x]:
         f3 = config_fields("cfg3", (n, n, n))
         w3 = quantize(tab.lookup(10, 512)).weight_sequence
-        for fuse3 in (1, 2):
+        for fuse3 in (1, 2, 3):
             ms, g, frac = measure(f3, w3, 48, fuse3)
             print(json.dumps(dict(kind="3d", n=n, fuse=fuse3, ms_per_sweep=ms, glups=g,
                                   frac_alg=frac)), flush=True)
     if not a.nl:
         return
     f5 = config_fields("cfg5", (256, 256, 256))
-    w5 = quantize(tab.lookup(8, 256)).weight_sequence
+    w5 = config_schedule("cfg5").weight_sequence
     ms, g, frac = measure(f5, w5, 48, 0)
     print(json.dumps(dict(kind="3d-nl", n=256, ms_per_sweep=ms, glups=g, frac_alg=frac)), flush=True)
 
