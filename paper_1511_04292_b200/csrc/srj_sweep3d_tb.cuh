@@ -37,7 +37,10 @@ struct Sweep3DTBParams {
 
 template <int T>
 struct Tile3D {
-  static constexpr int TJ = 16, TK = 64;                 // owned cells per tile
+  // T=2: two 256-thread CTAs per SM (113 KB of shared memory each) so one
+  // CTA computes while the other drains its stage barrier; T=3 needs the
+  // whole shared memory for one 512-thread CTA.
+  static constexpr int TJ = T == 2 ? 12 : 16, TK = 64;  // owned cells per tile
   static constexpr int HJ = TJ + 2 * T, HK = TK + 2 * T; // loaded tile
   // A TMA box must start on a 16-B aligned column (an fp64 box at an odd
   // column faults): for odd T the box starts one column left of the tile
@@ -47,7 +50,11 @@ struct Tile3D {
   static constexpr int HS = (HK + KOFF + 1) / 2 * 2;
   static constexpr int L = (T > 2 ? T : 2);              // ticks a slot stays live
   static constexpr int NS = L + 3;                       // slots: prefetch 2 planes
-  static constexpr int THREADS = 512;
+  static constexpr int THREADS = T == 2 ? 256 : 512;
+  static constexpr int MINB = T == 2 ? 2 : 1;  // resident CTAs per SM
+  // cell slots per thread: stage 1 has the largest region
+  static constexpr int UM = ((HJ - 2) * (HK - 2) + THREADS - 1) / THREADS;
+  static_assert(UM <= 8, "flag bits hold 8 slots");
   static constexpr int BOX_BYTES = HJ * HS * 8;          // one TMA box (u or f)
   // slot stride padded to 128 B: every TMA destination must be 128-B aligned
   static constexpr int TILE = (HJ * HS + 15) / 16 * 16;  // doubles per slot
@@ -59,7 +66,7 @@ struct Tile3D {
 };
 
 template <int T, bool NL, bool RECIP>
-__global__ void __launch_bounds__(Tile3D<T>::THREADS, 1)
+__global__ void __launch_bounds__(Tile3D<T>::THREADS, Tile3D<T>::MINB)
     sweep3d_tb(const __grid_constant__ Sweep3DTBParams p, const __grid_constant__ CUtensorMap tm_u,
                const __grid_constant__ CUtensorMap tm_f) {
   using B = Tile3D<T>;
@@ -110,6 +117,34 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, 1)
   }
   __syncthreads();
 
+  // Tick-invariant cell slots: stage t's region (the tile shrunk by t per
+  // side) is dealt round-robin to the threads, at most UM cells per thread.
+  // Offsets, grid-bounds and owned flags are computed once per CTA.
+  constexpr int UM = B::UM;
+  int off[T][UM];        // smem offset of the cell, -1 for an empty slot
+  unsigned flg[T];       // bit u: inside the grid; bit 8+u: owned (tile interior)
+  int64_t goff[UM];      // stage T: global offset of the cell within its plane
+#pragma unroll
+  for (int t = 1; t <= T; ++t) {
+    const int RJ = HJ - 2 * t, RK = HK - 2 * t, NC = RJ * RK;
+    flg[t - 1] = 0u;
+#pragma unroll
+    for (int u = 0; u < UM; ++u) {
+      const int q = tid + u * B::THREADS;
+      off[t - 1][u] = -1;
+      if (t == T) goff[u] = 0;
+      if (q < NC) {
+        const int jj = t + q / RK, kk = t + q % RK;
+        const int j = j0 + jj, k = k0 + kk;
+        off[t - 1][u] = jj * HS + kk + KOFF;
+        const bool inb = j >= 0 && j < p.n1 && k >= 0 && k < p.n2;
+        const bool own = inb && jj >= T && jj < T + TJ && kk >= T && kk < T + TK;
+        flg[t - 1] |= (inb ? 1u << u : 0u) | (own ? 1u << (8 + u) : 0u);
+        if (t == T) goff[u] = int64_t(j) * p.pitch + k;
+      }
+    }
+  }
+
   double rmx[T];  // dmax follows from rmax (monotone map, constant stencil)
 #pragma unroll
   for (int t = 0; t < T; ++t) rmx[t] = 0.0;
@@ -135,64 +170,50 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, 1)
       }
       const double *fp = ring_f + ((it - t + 2 * NS) % NS) * TILE;
       double *out = (t < T) ? win + (t - 1) * 3 * TILE + ((pl % 3 + 3) % 3) * TILE : nullptr;
-      const bool plane_act = (pl >= 0) && (pl < p.n0);
-      const bool plane_own = (pl >= i0) && (pl < i1);
-      const int RJ = HJ - 2 * t, RK = HK - 2 * t;  // stage region (t unrolled)
+      // whole-plane predicates fold into the per-cell flags
+      const unsigned pa = (pl >= 0 && pl < p.n0) ? 0xffu : 0u;
+      const unsigned po = (pl >= i0 && pl < i1) ? 0xffu : 0u;
+      const unsigned act_m = flg[t - 1] & pa;
+      const unsigned own_m = (flg[t - 1] >> 8) & pa & po;
       const double om = p.omega[t - 1];
-      // 4 independent cells per thread per iteration (ILP); one warp vote per
-      // iteration for the rare numerators outside div_recip's range
-      constexpr int U = 4;
-      const int NCELL = RJ * RK, ITER = (NCELL + U * B::THREADS - 1) / (U * B::THREADS);
-#pragma unroll 1
-      for (int itr = 0; itr < ITER; ++itr) {
-        double y[U], num[U], uc[U];
-        bool act[U], own[U], bad = false;
-        int o[U];
+      double y[UM], num[UM], uc[UM];
+      bool bad = false;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int q = tid + (itr * U + u) * B::THREADS;
-          const bool in = q < NCELL;
-          const int jj = t + (in ? q : 0) / RK, kk = t + (in ? q : 0) % RK;
-          o[u] = jj * HS + kk + KOFF;
-          const int j = j0 + jj, k = k0 + kk;
-          uc[u] = md[o[u]];
-          act[u] = in && plane_act && j >= 0 && j < p.n1 && k >= 0 && k < p.n2;
-          own[u] = act[u] && plane_own && jj >= T && jj < T + TJ && kk >= T && kk < T + TK;
-          y[u] = uc[u];
-          num[u] = 1.0;
-          if (act[u]) {
-            const double sv = NL ? nl_source(fp[o[u]], uc[u]) : fp[o[u]];
-            const double rr = resid7(sv, p.kc[0], uc[u], p.kc[1], up[o[u]], p.kc[2], dn[o[u]],
-                                     p.kc[3], md[o[u] - HS], p.kc[4], md[o[u] + HS], p.kc[5],
-                                     md[o[u] - 1], p.kc[6], md[o[u] + 1]);
-            num[u] = __dmul_rn(om, rr);
-            double d;
-            if (RECIP) {
-              d = div_recip(num[u], p.kc[0], p.kinv, p.kinv_lo);
-              bad |= recip_unsafe(num[u]);
-            } else {
-              d = __ddiv_rn(num[u], p.kc[0]);
-            }
-            y[u] = __dadd_rn(uc[u], d);
-            if (own[u]) acc_max(rmx[t - 1], rr);
-          }
+      for (int u = 0; u < UM; ++u) {
+        const int o = off[t - 1][u];
+        if (o < 0) continue;
+        // branch-free: every slot is computed, inactive ones keep their value
+        uc[u] = md[o];
+        const bool a = (act_m >> u) & 1u;
+        const double sv = NL ? nl_source(fp[o], uc[u]) : fp[o];
+        const double rr = resid7(sv, p.kc[0], uc[u], p.kc[1], up[o], p.kc[2], dn[o], p.kc[3],
+                                 md[o - HS], p.kc[4], md[o + HS], p.kc[5], md[o - 1], p.kc[6],
+                                 md[o + 1]);
+        num[u] = __dmul_rn(om, rr);
+        double d;
+        if (RECIP) {
+          d = div_recip(num[u], p.kc[0], p.kinv, p.kinv_lo);
+          bad |= a && recip_unsafe(num[u]);
+        } else {
+          d = __ddiv_rn(num[u], p.kc[0]);
         }
-        if (RECIP && __any_sync(kFull, bad)) {
+        y[u] = a ? __dadd_rn(uc[u], d) : uc[u];
+        if ((own_m >> u) & 1u) acc_max(rmx[t - 1], rr);
+      }
+      if (RECIP && __any_sync(kFull, bad)) {
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (act[u] && recip_unsafe(num[u]))
-              y[u] = __dadd_rn(uc[u], div_ieee(num[u], p.kc[0]));
-        }
+        for (int u = 0; u < UM; ++u)
+          if (off[t - 1][u] >= 0 && (act_m & (1u << u)) && recip_unsafe(num[u]))
+            y[u] = __dadd_rn(uc[u], div_ieee(num[u], p.kc[0]));
+      }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int q = tid + (itr * U + u) * B::THREADS;
-          if (q >= NCELL) continue;
-          if (t < T) {
-            out[o[u]] = y[u];
-          } else if (own[u]) {
-            const int jj = (o[u] - KOFF) / HS, kk = (o[u] - KOFF) % HS;
-            p.dst[int64_t(pl) * p.plane + int64_t(j0 + jj) * p.pitch + (k0 + kk)] = y[u];
-          }
+      for (int u = 0; u < UM; ++u) {
+        const int o = off[t - 1][u];
+        if (o < 0) continue;
+        if (t < T) {
+          out[o] = y[u];
+        } else if (own_m & (1u << u)) {
+          p.dst[int64_t(pl) * p.plane + goff[u]] = y[u];
         }
       }
       __syncthreads();
@@ -203,7 +224,6 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, 1)
       issue(it - B::L + NS);
     }
   }
-
   // per-step norms: warp max, then one atomic per warp
 #pragma unroll
   for (int t = 0; t < T; ++t) {

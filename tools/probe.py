@@ -73,8 +73,10 @@ def main():
         return
     f5 = config_fields("cfg5", (256, 256, 256))
     w5 = config_schedule("cfg5").weight_sequence
-    ms, g, frac = measure(f5, w5, 48, 0)
-    print(json.dumps(dict(kind="3d-nl", n=256, ms_per_sweep=ms, glups=g, frac_alg=frac)), flush=True)
+    for fuse5 in (1, 2, 3):
+        ms, g, frac = measure(f5, w5, 48, fuse5)
+        print(json.dumps(dict(kind="3d-nl", n=256, fuse=fuse5, ms_per_sweep=ms, glups=g,
+                              frac_alg=frac)), flush=True)
 
 
 if __name__ == "__main__":
