@@ -13,7 +13,7 @@ import pytest
 
 import oracle
 from conftest import fields_from, load_golden
-from helpers import Cycle, problem_from
+from helpers import Cycle, crop_window, problem_from
 from paper_1511_04292_b200 import grids as G
 from paper_1511_04292_b200.problems import config_fields, nonlinear_fields
 from paper_1511_04292_b200.schedule import quantize
@@ -516,3 +516,35 @@ def test_edge_shapes_variable_and_masked(shape):
     hist, _ = run_steps(p, w, 40, chunk=9)
     assert np.array_equal(p.u, want.u)
     assert np.array_equal(hist.true_residual_inf, norms[:, 1])
+
+
+@pytest.mark.parametrize("name,steps,fuse", [("cfg4", 12, 4), ("cfg3", 6, 2)])
+def test_full_size_windows_vs_cropped_oracle(name, steps, fuse):
+    """BASELINE's largest single-GPU layouts (cfg4 32768^2: 1.08e9 elements
+    per buffer; cfg3 512^3): k sweeps of the real schedule at full size,
+    windows at the low corner (true boundary), the middle and the far corner
+    (largest offsets) bitwise against the oracle on cropped sub-problems."""
+    psutil = pytest.importorskip("psutil")
+    need = 40e9 if name == "cfg4" else 8e9
+    if psutil.virtual_memory().available < need:
+        pytest.skip("not enough host memory for the full-size fields")
+    from paper_1511_04292_b200.grids import FIXED, GridProblem
+    from paper_1511_04292_b200.problems import config_schedule
+
+    f = config_fields(name)
+    w = config_schedule(name).weight_sequence
+    shape = f["source"].shape
+    nd = len(shape)
+    ext = 48 if nd == 2 else 12
+    wins = [([0] * nd, [ext] * nd),
+            ([n // 2 - ext // 2 for n in shape], [n // 2 + ext // 2 for n in shape]),
+            ([n - ext for n in shape], list(shape))]
+    crops = [crop_window(f, lo, hi, steps) for lo, hi in wins]
+    p = GridProblem(spacing=(1.0,) * nd, u=f["u"], source=f["source"], center=f["center"],
+                    lower=f["lower"], upper=f["upper"], bc=((FIXED, FIXED),) * nd)
+    run_steps(p, w, steps, fuse=fuse)
+    for (lo, hi), (sub, win) in zip(wins, crops):
+        q = problem_from(sub)
+        oracle.run(q, w, 0, steps)
+        full = p.u[tuple(slice(l + 1, h + 1) for l, h in zip(lo, hi))]
+        assert np.array_equal(full, q.u[tuple(slice(s.start + 1, s.stop + 1) for s in win)]), (lo, hi)

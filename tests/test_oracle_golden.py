@@ -129,3 +129,26 @@ def test_oracle_boundary_rules_match_reference(name):
     metric = norms[:, 0] / np.abs(g["weights"][np.arange(steps) % len(g["weights"])])
     assert np.array_equal(metric, g["residual_inf"])
     assert np.array_equal(norms[:, 1], g["true_residual_inf"])
+
+
+@pytest.mark.parametrize("name,shape,k", [("cfg4", (120, 97), 6), ("cfg3", (22, 18, 30), 3)])
+def test_dependency_cone_crops(name, shape, k):
+    """The crop construction the full-size GPU tests rely on: after k sweeps
+    the window of a cropped sub-problem equals the full grid's; the stale
+    ghost ring (k+1 cells out) first reaches the window at sweep k+2."""
+    from helpers import crop_window, problem_from
+    from paper_1511_04292_b200.problems import config_fields, config_schedule
+
+    f = config_fields(name, shape)
+    w = config_schedule(name).weight_sequence
+    nd = len(shape)
+    lo, hi = [n // 2 - 4 for n in shape], [n // 2 + 4 for n in shape]
+    sub, win = crop_window(f, lo, hi, k)
+    for steps, same in ((k, True), (k + 1, True), (k + 2, False)):
+        p, q = problem_from(f), problem_from(sub)
+        oracle.run(p, w, 0, steps)
+        oracle.run(q, w, 0, steps)
+        a = p.u[tuple(slice(l + 1, h + 1) for l, h in zip(lo, hi))]
+        b = q.u[tuple(slice(s.start + 1, s.stop + 1) for s in win)]
+        assert np.array_equal(a, b) == same
+    assert nd == len(win)
