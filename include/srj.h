@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SRJ_ABI_VERSION 2
+#define SRJ_ABI_VERSION 3
 
 enum {
     SRJ_OK = 0,
@@ -134,6 +134,18 @@ typedef struct srj_plan srj_plan;
 /* Validates the descriptor, allocates small device scratch. */
 int srj_plan_create(const srj_plan_desc *desc, srj_plan **out);
 int srj_plan_destroy(srj_plan *plan);
+
+/* Post-sweep gather: the device form of the reference's `post_sweep` hooks
+ * that copy field values (GridProblem.post_sweep, grids.py:146-163, called by
+ * refresh_ghosts :246-247; e.g. the spherical tie_origin u[1] = u[2],
+ * u[0] = u[2], problems.py:586-589).  After every sweep and its ghost
+ * refresh, field[dst[i]] = field[src[i]] for i < n with simultaneous
+ * semantics (all sources read before any destination is written).  dst/src
+ * are HOST arrays of element offsets from the start of a field buffer in the
+ * padded layout; the plan keeps a device copy.  n = 0 removes the gather.
+ * Like a non-FIXED face, it makes every launch a single sweep. */
+int srj_plan_set_post_gather(srj_plan *plan, const int64_t *dst,
+                             const int64_t *src, int64_t n);
 
 /* Maximum fused-sweep depth (temporal blocking) supported by srj_plan_run. */
 int srj_max_fuse(void);

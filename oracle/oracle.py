@@ -286,8 +286,9 @@ def refresh_ghosts(u, bc):
             u[face(ax, n - 1)] = 2.0 * vhi - u[face(ax, n - 2)]
 
 
-def run_bc(problem, bc, weights, nsteps, tol=0.0, kappa=None):
-    """Step-by-step solve with a ghost refresh after every step (any bc).
+def run_bc(problem, bc, weights, nsteps, tol=0.0, kappa=None, post=None):
+    """Step-by-step solve with a ghost refresh after every step (any bc),
+    followed by the ``post_sweep`` hook ``post`` when given (grids.py:246-247).
 
     Same stopping semantics as ``run`` (grids.py:613-628); returns
     (steps, status, norms[steps, 2]).
@@ -299,6 +300,8 @@ def run_bc(problem, bc, weights, nsteps, tol=0.0, kappa=None):
         omega = w[k % len(w)]
         dm, rm = step(problem, omega, kappa=kappa)
         refresh_ghosts(problem.u, bc)
+        if post is not None:
+            post(problem.u)
         norms.append((dm, rm))
         if tol != 0.0:
             metric = dm / abs(omega)

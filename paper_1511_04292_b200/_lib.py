@@ -17,7 +17,7 @@ SRJ_EINVAL = -1
 SRJ_ECUDA = -2
 SRJ_ENOMEM = -3
 SRJ_EUNSUPPORTED = -4
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 BC_KINDS = {"fixed": 0, "mirror": 1, "periodic": 2, "face_dirichlet": 3}
 
@@ -78,6 +78,8 @@ _SIGNATURES = {
     "srj_plan_create": (ctypes.c_int, [ctypes.POINTER(SrjPlanDesc),
                                        ctypes.POINTER(ctypes.c_void_p)]),
     "srj_plan_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "srj_plan_set_post_gather": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_int64]),
     "srj_plan_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p, _c_dp, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,

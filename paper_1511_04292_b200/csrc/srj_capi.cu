@@ -305,7 +305,29 @@ struct srj_plan {
   double *d_omegas = nullptr, *h_omegas = nullptr;
   int64_t omega_cap = 0;
   cudaEvent_t omega_ev = nullptr;
+  // post-sweep gather (device copies; tmp only when dst and src overlap)
+  int64_t *g_dst = nullptr, *g_src = nullptr;
+  double *g_tmp = nullptr;
+  int64_t g_n = 0;
 };
+
+static void free_gather(srj_plan *p) {
+  if (p->g_dst) cudaFree(p->g_dst);
+  if (p->g_src) cudaFree(p->g_src);
+  if (p->g_tmp) cudaFree(p->g_tmp);
+  p->g_dst = p->g_src = nullptr;
+  p->g_tmp = nullptr;
+  p->g_n = 0;
+}
+
+static int launch_gather(const srj_plan &plan, double *field, cudaStream_t st) {
+  const int blocks = int(std::min<int64_t>((plan.g_n + 255) / 256, int64_t(sm_count()) * 8));
+  post_gather<<<blocks, 256, 0, st>>>(field, plan.g_dst, plan.g_src, plan.g_n, plan.g_tmp, 0);
+  if (plan.g_tmp)
+    post_gather<<<blocks, 256, 0, st>>>(field, plan.g_dst, plan.g_src, plan.g_n, plan.g_tmp, 1);
+  SRJ_CUDA(cudaGetLastError());
+  return SRJ_OK;
+}
 
 extern "C" {
 
@@ -434,8 +456,41 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
   return SRJ_OK;
 }
 
+int srj_plan_set_post_gather(srj_plan *p, const int64_t *dst, const int64_t *src, int64_t n) {
+  if (!p) return fail(SRJ_EINVAL, "null plan");
+  if (n < 0 || (n > 0 && (!dst || !src))) return fail(SRJ_EINVAL, "bad gather arguments");
+  free_gather(p);
+  if (n == 0) return SRJ_OK;
+  const srj_layout_t &l = p->d.layout;
+  if (!p->d.physical_lo0 || !p->d.physical_hi0 || p->d.own0_begin != 0 || p->d.own0_end != l.n[0])
+    return fail(SRJ_EUNSUPPORTED, "post-sweep gathers need the whole grid on one plan");
+  std::vector<int64_t> sorted_dst(dst, dst + n);
+  for (int64_t i = 0; i < n; ++i)
+    if (dst[i] < 0 || dst[i] >= l.elems || src[i] < 0 || src[i] >= l.elems)
+      return fail(SRJ_EINVAL, "gather offset %lld out of range", (long long)i);
+  std::sort(sorted_dst.begin(), sorted_dst.end());
+  if (std::adjacent_find(sorted_dst.begin(), sorted_dst.end()) != sorted_dst.end())
+    return fail(SRJ_EINVAL, "gather destinations must be distinct");
+  bool overlap = false;
+  for (int64_t i = 0; i < n && !overlap; ++i)
+    overlap = std::binary_search(sorted_dst.begin(), sorted_dst.end(), src[i]);
+  const size_t bytes = sizeof(int64_t) * size_t(n);
+  cudaError_t e = cudaMalloc(&p->g_dst, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&p->g_src, bytes);
+  if (e == cudaSuccess && overlap) e = cudaMalloc(&p->g_tmp, sizeof(double) * size_t(n));
+  if (e == cudaSuccess) e = cudaMemcpy(p->g_dst, dst, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->g_src, src, bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    free_gather(p);
+    return cuda_fail(e, "post-gather setup");
+  }
+  p->g_n = n;
+  return SRJ_OK;
+}
+
 int srj_plan_destroy(srj_plan *p) {
   if (!p) return SRJ_OK;
+  free_gather(p);
   if (p->partials) cudaFree(p->partials);
   if (p->d_omegas) cudaFree(p->d_omegas);
   if (p->h_omegas) cudaFreeHost(p->h_omegas);
@@ -638,7 +693,7 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
   const srj_layout_t &l = d.layout;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int T = fuse > 0 ? fuse : plan->default_fuse;
-  if (plan->has_bc || (l.ndim == 3 && d.coef_mode == 1)) T = 1;
+  if (plan->has_bc || plan->g_n > 0 || (l.ndim == 3 && d.coef_mode == 1)) T = 1;
   if (l.ndim == 3 && T > kMaxFuse3D) T = kMaxFuse3D;
   if (T > kMaxFuse) return fail(SRJ_EINVAL, "fuse depth %d exceeds %d", T, kMaxFuse);
   if ((!d.physical_lo0 || !d.physical_hi0) && T > l.halo0)
@@ -653,7 +708,7 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
   row_ranges(d, lo_c, hi_c, ld_lo, ld_hi);
   const int rows = int(d.own0_end - d.own0_begin);
 
-  if (l.ndim == 2) {
+  if (l.ndim == 2 && plan->g_n == 0) {
     int C = 0, R = 0;
     if (cluster_fits(*plan, C, R)) return run_cluster2d(*plan, src, buf_a, weights, m, first, nsteps, d_norms, final_buf, st, C, R);
   }
@@ -813,6 +868,10 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
     SRJ_CUDA(cudaGetLastError());
     if (plan->has_bc) {
       const int rc = launch_ghosts(d, nxt + ioff, st);
+      if (rc != SRJ_OK) return rc;
+    }
+    if (plan->g_n > 0) {
+      const int rc = launch_gather(*plan, nxt, st);
       if (rc != SRJ_OK) return rc;
     }
     k += t;

@@ -164,6 +164,22 @@ __global__ void __launch_bounds__(256) ghost_refresh(const __grid_constant__ Gho
   }
 }
 
+// Post-sweep gather (srj_plan_set_post_gather): phase 0 copies (or stages
+// into tmp when destinations overlap sources), phase 1 scatters tmp.
+__global__ void __launch_bounds__(256)
+    post_gather(double *u, const int64_t *dst, const int64_t *src, int64_t n, double *tmp,
+                int phase) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    if (phase == 1)
+      u[dst[i]] = tmp[i];
+    else if (tmp)
+      tmp[i] = u[src[i]];
+    else
+      u[dst[i]] = u[src[i]];
+  }
+}
+
 struct DenseParams {
   const double *u;
   double *un;

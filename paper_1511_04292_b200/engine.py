@@ -64,7 +64,8 @@ class DeviceGrid:
     """
 
     def __init__(self, u, source, center, lower, upper, active=None, kappa=None,
-                 halo0=1, own=None, physical=(True, True), device=None, bc=None):
+                 halo0=1, own=None, physical=(True, True), device=None, bc=None,
+                 post_gather=None):
         torch = require_cuda()
         lib = _lib.load()
         self.torch = torch
@@ -128,8 +129,28 @@ class DeviceGrid:
             _lib.check(lib.srj_plan_create(ctypes.byref(desc), ctypes.byref(plan)),
                        "srj_plan_create")
             self.plan = plan
+            if post_gather is not None and len(post_gather[0]):
+                self._set_post_gather(*post_gather)
             self.norms = torch.zeros(2, dtype=torch.float64, device=self.device)
             self.resid_out = torch.zeros(2, dtype=torch.float64, device=self.device)
+
+    def _set_post_gather(self, dst, src):
+        """Install a post-sweep gather given as flat indices of the ghosted
+        field (C order, shape n+2 per axis); converted to padded offsets."""
+        lay = self.layout
+        gshape = tuple(n + 2 for n in self.shape)
+
+        def offsets(flat):
+            idx = np.unravel_index(np.asarray(flat, dtype=np.int64), gshape)
+            off = int(lay.origin) + (int(lay.halo0) - 1 + idx[0]) * int(lay.plane)
+            if self.ndim == 3:
+                off = off + idx[1] * int(lay.pitch)
+            return np.ascontiguousarray(off + idx[-1], dtype=np.int64)
+
+        d, s = offsets(dst), offsets(src)
+        _lib.check(self.lib.srj_plan_set_post_gather(
+            self.plan, d.ctypes.data_as(ctypes.c_void_p), s.ctypes.data_as(ctypes.c_void_p),
+            len(d)), "srj_plan_set_post_gather")
 
     def _set_face(self, face, rule, ax):
         """Fill one srj_face_rule from a reference BoundaryRule (grids.py:73-112)."""

@@ -11,9 +11,11 @@ GPU scope: 2-D 5-point and 3-D 7-point stencils with
 every reference boundary rule (FIXED ghosts run fused multi-sweep kernels;
 mirror / periodic / face-Dirichlet faces run one sweep per launch followed by
 a device ghost refresh), constant or per-cell coefficients, optional mask,
-optional nonlinear source.  ``post_sweep`` hooks (arbitrary Python), 1-D grids
-and the Gauss-Seidel/SOR solvers raise ``NotImplementedError`` -- there is no
-CPU fallback.
+optional nonlinear source, ``post_sweep`` hooks that copy field values (e.g.
+the spherical ``tie_origin``; applied on the device as a gather after every
+sweep, ``post_sweep_gather``).  Hooks that compute values, 1-D grids and the
+Gauss-Seidel/SOR solvers raise ``NotImplementedError`` -- there is no CPU
+fallback.
 
 Entry points and the reference code they replace:
 
@@ -273,14 +275,62 @@ def _device_grid(problem):
         for rule in pair:
             if rule.kind not in ("fixed", "mirror", "periodic", "face_dirichlet"):
                 raise NotImplementedError(f"boundary kind {rule.kind!r} is not on the GPU path")
+    gather = None
     if getattr(problem, "post_sweep", None) is not None:
-        raise NotImplementedError("post_sweep hooks are not on the GPU path")
+        gather = post_sweep_gather(problem.post_sweep, problem.u.shape)
     active = getattr(problem, "_active", None)
     if active is None:
         active = getattr(problem, "mask", None)
     kappa = getattr(problem, "source_kappa", None)
     return DeviceGrid(problem.u, problem.source, problem.center, problem.lower,
-                      problem.upper, active=active, kappa=kappa, bc=problem.bc)
+                      problem.upper, active=active, kappa=kappa, bc=problem.bc,
+                      post_gather=gather)
+
+
+def post_sweep_gather(hook, shape):
+    """Express a ``post_sweep`` hook (``grids.py:146-163``, called at the end
+    of ``refresh_ghosts`` :246-247) as a gather ``u[dst] = u[src]`` with
+    simultaneous semantics, so the device can apply it after every sweep.
+
+    The hook is probed on copies of the ghosted field: two arrays of unique
+    values (identity and a random permutation) must agree on which flat
+    positions change and which position each new value came from, and a
+    random-valued array must then be reproduced exactly by that gather, so a
+    hook that computes (rather than copies) values is rejected.  Returns
+    (dst, src) int64 flat indices; raises ``NotImplementedError`` otherwise.
+    E.g. the spherical ``tie_origin`` (``problems.py:586-589``).
+    """
+    shape = tuple(int(n) for n in shape)
+    n = int(np.prod(shape))
+    if n >= 2 ** 52:
+        raise NotImplementedError("field too large to probe the post_sweep hook")
+    rng = np.random.default_rng(1234)
+    maps = []
+    for perm in (np.arange(n), rng.permutation(n)):
+        a = perm.astype(np.float64).reshape(shape)
+        try:
+            hook(a)
+        except Exception as exc:  # noqa: BLE001 - any failure means "not a gather"
+            raise NotImplementedError(f"post_sweep hook could not be probed: {exc}") from exc
+        flat = a.reshape(-1)
+        dst = np.flatnonzero(flat != perm)
+        vals = flat[dst]
+        if not (np.all(vals == np.rint(vals)) and np.all((vals >= 0) & (vals < n))):
+            raise NotImplementedError("post_sweep hook is not a copy of field values")
+        inv = np.empty(n, dtype=np.int64)
+        inv[perm] = np.arange(n)
+        maps.append((dst.astype(np.int64), inv[vals.astype(np.int64)]))
+    (d0, s0), (d1, s1) = maps
+    if not (np.array_equal(d0, d1) and np.array_equal(s0, s1)):
+        raise NotImplementedError("post_sweep hook is not a fixed gather of field values")
+    x = rng.standard_normal(shape)
+    want = x.copy()
+    hook(want)
+    got = x.copy().reshape(-1)
+    got[d0] = x.reshape(-1)[s0]
+    if not np.array_equal(got.reshape(shape), want):
+        raise NotImplementedError("post_sweep hook is not a fixed gather of field values")
+    return d0, s0
 
 
 def _step_seconds_estimate(problem):
@@ -296,10 +346,9 @@ def weighted_jacobi_sweep(problem, omega, traversal="forward"):
     try:
         out = dev.run(0, np.array([float(omega)]), 0, 1, fuse=1)
         norms = dev.norms[:2].cpu().numpy()
-        dev.download_field(out, problem.u)
+        dev.download_field(out, problem.u)  # ghosts refreshed on the device
     finally:
         dev.close()
-    problem.refresh_ghosts()
     return float(norms[0]), float(norms[1])
 
 
@@ -377,10 +426,9 @@ def _solve(problem, weights, tol, max_iters, normalise, stop, check_every, fuse,
                 if rel < tol:
                     converged = True
                     break
-        dev.download_field(cur, problem.u)
+        dev.download_field(cur, problem.u)  # ghosts refreshed on the device
     finally:
         dev.close()
-    problem.refresh_ghosts()
     hist = ResidualHistory(
         residual_inf=np.concatenate(diffs) if diffs else np.zeros(0),
         true_residual_inf=np.concatenate(resids) if resids else np.zeros(0),

@@ -67,3 +67,18 @@ def rules_from(g):
                          else G.BoundaryRule(kind))
         out.append(tuple(rules))
     return tuple(out)
+
+
+def tie_origin(uu):
+    """The spherical problems' inner-radius tie u_0 = u_1 = u_2 (a
+    ``post_sweep`` hook, restated from the reference problems.py:586-589)."""
+    uu[1] = uu[2]
+    uu[0] = uu[2]
+
+
+POST_HOOKS = {"tie_origin": tie_origin}
+
+
+def post_from(g):
+    """The post_sweep hook a boundary fixture was generated with, or None."""
+    return POST_HOOKS[str(g["post"])] if "post" in g else None

@@ -5,7 +5,7 @@ import numpy as np
 from paper_1511_04292_b200.grids import FIXED, GridProblem
 
 
-def problem_from(fields, kappa=None, bc=None):
+def problem_from(fields, kappa=None, bc=None, post=None):
     nd = fields["source"].ndim
     if bc is not None:
         from paper_1511_04292_b200.grids import GridProblem as GP
@@ -15,7 +15,7 @@ def problem_from(fields, kappa=None, bc=None):
                   center=np.asarray(fields["center"], dtype=float),
                   lower=tuple(np.asarray(a, dtype=float) for a in fields["lower"]),
                   upper=tuple(np.asarray(a, dtype=float) for a in fields["upper"]),
-                  bc=bc, mask=fields.get("mask"))
+                  bc=bc, mask=fields.get("mask"), post_sweep=post)
     return GridProblem(
         spacing=(1.0,) * nd,
         u=np.array(fields["u"], dtype=float, copy=True),

@@ -341,17 +341,19 @@ def test_slab_decomposition_3d_on_one_gpu(table, fuse):
 
 
 # ------------------------------------------- non-FIXED boundary rules on GPU
-BC_CASES = ["neumann2d", "periodic2d", "facedir3d", "gs_a", "gs_b"]
+BC_CASES = ["neumann2d", "periodic2d", "facedir3d", "gs_a", "gs_b", "spherical2d",
+            "spherical3d"]
 
 
 @pytest.mark.parametrize("name", BC_CASES)
 def test_boundary_rules_bitwise_vs_reference(name):
     """mirror / periodic / face-Dirichlet (scalar and array) ghosts refreshed on
-    the device after every sweep == the reference srj_solve bit for bit."""
-    from conftest import rules_from
+    the device after every sweep (and the spherical tie_origin post_sweep hook
+    as a device gather) == the reference srj_solve bit for bit."""
+    from conftest import post_from, rules_from
 
     g = load_golden(name)
-    p = problem_from(fields_from(g), bc=rules_from(g))
+    p = problem_from(fields_from(g), bc=rules_from(g), post=post_from(g))
     hist, _ = run_steps(p, g["weights"], int(g["steps"]), chunk=77)
     assert np.array_equal(p.u, g["u_final"])
     assert np.array_equal(hist.residual_inf, g["residual_inf"])
@@ -398,7 +400,7 @@ def test_band_kernels_without_cluster_path():
     here = os.path.dirname(os.path.abspath(__file__))
     res = subprocess.run(
         [sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", os.path.join(here, "test_gpu_parity.py"),
-         "-k", "not band_kernels_without and not reciprocal"],
+         "-k", "not band_kernels_without and not reciprocal and not full_size_windows"],
         env=env, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
 
@@ -548,3 +550,26 @@ def test_full_size_windows_vs_cropped_oracle(name, steps, fuse):
         oracle.run(q, w, 0, steps)
         full = p.u[tuple(slice(l + 1, h + 1) for l, h in zip(lo, hi))]
         assert np.array_equal(full, q.u[tuple(slice(s.start + 1, s.stop + 1) for s in win)]), (lo, hi)
+
+
+def test_post_sweep_gather_overlapping_vs_oracle(table):
+    """A post_sweep hook whose destinations are also sources (staged through
+    the plan's temporary) on a masked 3D problem with mirror ghosts."""
+    from paper_1511_04292_b200.grids import FIXED, MIRROR
+
+    def chain(uu):
+        uu[0] = uu[1]
+        uu[1] = uu[2]
+        uu[:, 0] = uu[:, 3]
+
+    g = load_golden("var3d_mask")
+    f = fields_from(g)
+    bc = ((FIXED, FIXED), (MIRROR, MIRROR), (FIXED, FIXED))
+    p = problem_from(f, bc=bc, post=chain)
+    w = g["weights"]
+    hist, _ = run_steps(p, w, 90)
+    q = problem_from(f, bc=bc, post=chain)
+    spec = tuple(((r.kind, None), (s.kind, None)) for r, s in bc)
+    _, _, norms = oracle.run_bc(q, spec, w, 90, post=chain)
+    assert np.array_equal(p.u, q.u)
+    assert np.array_equal(hist.true_residual_inf, norms[:, 1])

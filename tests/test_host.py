@@ -110,7 +110,11 @@ def test_unsupported_features_raise():
     with pytest.raises(NotImplementedError):
         G.srj_solve(p, type("C", (), {"weight_sequence": np.ones(1)})(), 1e-6)
     q = G.GridProblem(**_kw((4, 4), bc=((G.MIRROR, G.MIRROR),) * 2))
-    q.post_sweep = lambda u: None
+
+    def computing_hook(u):
+        u[0] = 2.0 * u[1] - u[2]
+
+    q.post_sweep = computing_hook
     with pytest.raises(NotImplementedError):
         G.jacobi_solve(q, 1e-6)
     with pytest.raises(NotImplementedError):
@@ -125,3 +129,41 @@ def test_no_cpu_fallback_without_cuda():
     p = G.GridProblem(**_kw((8, 8)))
     with pytest.raises(RuntimeError, match="CUDA"):
         G.jacobi_solve(p, 1e-6)
+
+
+def test_post_sweep_gather_probe():
+    """post_sweep hooks that copy values become a device gather (spherical
+    tie_origin, problems.py:586-589); anything else is rejected."""
+    shape = (6, 5, 7)
+
+    def tie_origin(uu):
+        uu[1] = uu[2]
+        uu[0] = uu[2]
+
+    dst, src = G.post_sweep_gather(tie_origin, shape)
+    plane = 5 * 7
+    assert np.array_equal(dst, np.arange(2 * plane))
+    assert np.array_equal(src, 2 * plane + np.arange(2 * plane) % plane)
+
+    def chain(uu):  # sequential copies -> simultaneous gather from originals
+        uu[0] = uu[1]
+        uu[1] = uu[2]
+
+    d, s = G.post_sweep_gather(chain, (4, 3))
+    assert np.array_equal(d, np.arange(6)) and np.array_equal(s, np.arange(3, 9))
+    x = np.random.default_rng(0).standard_normal((4, 3))
+    y = x.copy()
+    chain(y)
+    z = x.copy().reshape(-1)
+    z[d] = x.reshape(-1)[s]
+    assert np.array_equal(z.reshape(4, 3), y)
+
+    d, s = G.post_sweep_gather(lambda uu: None, (4, 3))
+    assert d.size == 0 and s.size == 0
+
+    for bad in (lambda uu: uu.__setitem__(0, 2.0 * uu[1]),
+                lambda uu: uu.__setitem__(0, uu[1] + 1.0),
+                lambda uu: uu.__setitem__(0, uu[1] if uu[1, 0] > 3 else uu[2]),
+                lambda uu: (_ for _ in ()).throw(RuntimeError("boom"))):
+        with pytest.raises(NotImplementedError):
+            G.post_sweep_gather(bad, (4, 3))

@@ -112,17 +112,18 @@ def test_oracle_nonlinear_source_restatement():
     assert oracle.residual(c, kappa=f["kappa"])[0] < r0
 
 
-BC_CASES = ["neumann2d", "periodic2d", "facedir3d", "gs_a", "gs_b", "gs_a_solve"]
+BC_CASES = ["neumann2d", "periodic2d", "facedir3d", "gs_a", "gs_b", "gs_a_solve",
+            "spherical2d", "spherical3d"]
 
 
 @pytest.mark.parametrize("name", BC_CASES)
 def test_oracle_boundary_rules_match_reference(name):
-    from conftest import bc_from
+    from conftest import bc_from, post_from
 
     g = load_golden(name)
     p = problem_from(fields_from(g))
     steps, status, norms = oracle.run_bc(p, bc_from(g), g["weights"], int(g["steps"]),
-                                         tol=float(g["tol"]))
+                                         tol=float(g["tol"]), post=post_from(g))
     assert steps == len(g["residual_inf"])
     assert status == (1 if bool(g["converged"]) else 0)
     assert np.array_equal(p.u, g["u_final"])

@@ -103,6 +103,45 @@ def fixed_steps(name, fields, weights, steps):
     save(name, **arrays)
 
 
+def bc_fixture(name, prob, weights, steps, tol=1e-300, post=None):
+    """Run the reference srj_solve on a full GridProblem (any bc)."""
+    nd = prob.ndim
+    arr = {"u0": prob.u.copy(), "source": prob.source.copy(),
+           "center": prob.center.copy()}
+    for ax in range(nd):
+        arr[f"lower{ax}"] = prob.lower[ax].copy()
+        arr[f"upper{ax}"] = prob.upper[ax].copy()
+        for side in range(2):
+            rule = prob.bc[ax][side]
+            arr[f"bc{ax}{side}"] = np.array(rule.kind)
+            if rule.kind == "face_dirichlet":
+                arr[f"bcval{ax}{side}"] = np.asarray(rule.values, dtype=float)
+    if prob.mask is not None:
+        arr["mask"] = prob.mask.copy()
+    if post is not None:  # name of the post_sweep hook the test restates
+        arr["post"] = np.array(post)
+
+    class _Cycle:
+        weight_sequence = np.asarray(weights, dtype=float)
+
+    hist, _ = G.srj_solve(prob, _Cycle(), tol=tol, max_iters=steps)
+    arr.update(weights=np.asarray(weights, dtype=float), steps=np.int64(steps),
+               tol=np.float64(tol), u_final=prob.u, residual_inf=hist.residual_inf,
+               true_residual_inf=hist.true_residual_inf,
+               converged=np.bool_(hist.converged))
+    save(name, **arr)
+
+
+def spherical_fixtures():
+    """Spherical Poisson (problems.py:443-600): mask + mirror/periodic ghosts +
+    the tie_origin post_sweep hook (u[1] = u[2], u[0] = u[2])."""
+    from srj.problems import spherical_poisson
+
+    w64 = quantize(shipped_table().get(6, 64).schedule).weight_sequence
+    bc_fixture("spherical2d", spherical_poisson(2, 16).problem, w64, 300, post="tie_origin")
+    bc_fixture("spherical3d", spherical_poisson(3, 10).problem, w64, 300, post="tie_origin")
+
+
 def main():
     table = shipped_table()
     rng = np.random.default_rng(20151113)
@@ -191,32 +230,6 @@ def main():
     # ---- non-FIXED boundary rules (BoundaryRule, grids.py:73-112) ---------
     from srj.problems import grad_shafranov, laplace2d_neumann
 
-    def bc_fixture(name, prob, weights, steps, tol=1e-300):
-        """Run the reference srj_solve on a full GridProblem (any bc)."""
-        nd = prob.ndim
-        arr = {"u0": prob.u.copy(), "source": prob.source.copy(),
-               "center": prob.center.copy()}
-        for ax in range(nd):
-            arr[f"lower{ax}"] = prob.lower[ax].copy()
-            arr[f"upper{ax}"] = prob.upper[ax].copy()
-            for side in range(2):
-                rule = prob.bc[ax][side]
-                arr[f"bc{ax}{side}"] = np.array(rule.kind)
-                if rule.kind == "face_dirichlet":
-                    arr[f"bcval{ax}{side}"] = np.asarray(rule.values, dtype=float)
-        if prob.mask is not None:
-            arr["mask"] = prob.mask.copy()
-
-        class _Cycle:
-            weight_sequence = np.asarray(weights, dtype=float)
-
-        hist, _ = G.srj_solve(prob, _Cycle(), tol=tol, max_iters=steps)
-        arr.update(weights=np.asarray(weights, dtype=float), steps=np.int64(steps),
-                   tol=np.float64(tol), u_final=prob.u, residual_inf=hist.residual_inf,
-                   true_residual_inf=hist.true_residual_inf,
-                   converged=np.bool_(hist.converged))
-        save(name, **arr)
-
     nm = laplace2d_neumann(24)
     nm.u[1:-1, 1:-1] = np.random.default_rng(3).standard_normal(nm.shape)
     nm.refresh_ghosts()
@@ -237,6 +250,7 @@ def main():
             (G.face_dirichlet(0.75), G.face_dirichlet(rng.standard_normal((9, 11))))))
     bc_fixture("facedir3d", fd, w64, 120)
 
+    spherical_fixtures()
     bc_fixture("gs_a", grad_shafranov("A", 0.0, 40), w64, 300)
     bc_fixture("gs_b", grad_shafranov("B", 0.0, 48), w64, 300)
     gs_row = table.lookup(14, 300)
@@ -277,4 +291,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["spherical"]:
+        spherical_fixtures()
+    else:
+        main()
