@@ -17,6 +17,7 @@ from .grids import (  # noqa: F401
     face_dirichlet,
     gauss_seidel_solve,
     jacobi_solve,
+    post_sweep_gather,
     sor_solve,
     srj_solve,
     weighted_jacobi_sweep,
