@@ -33,7 +33,7 @@ def problem(f):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="cfg1,cfg2,cfg3,cfg5")
-    ap.add_argument("--max-cycles", type=int, default=400)
+    ap.add_argument("--max-cycles", type=int, default=600)
     a = ap.parse_args()
     tab = shipped_table()
     plan = {
@@ -46,6 +46,7 @@ def main():
         cfg = CONFIGS[name]
         cyc = config_schedule(name, tab)
         f = config_fields(name)
+        G.srj_solve(problem(f), cyc, 1e-300, max_iters=16)  # warm-up: library, kernel setup
         for rule, tol in plan[name]:
             p = problem(f)
             torch.cuda.synchronize()
