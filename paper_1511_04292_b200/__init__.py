@@ -22,5 +22,6 @@ from .grids import (  # noqa: F401
     srj_solve,
     weighted_jacobi_sweep,
 )
+from .optimize import optimal_schedule  # noqa: F401
 from .schedule import CycleSchedule, WeightSchedule, quantize  # noqa: F401
 from .tables import shipped_table  # noqa: F401

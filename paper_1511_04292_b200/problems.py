@@ -47,8 +47,15 @@ CONFIGS = {
 }
 
 
-def config_schedule(name, table=None):
-    """The CycleSchedule a BASELINE config runs (floor quantization)."""
+def config_schedule(name, table=None, optimal=False):
+    """The CycleSchedule a BASELINE config runs (floor quantization).
+
+    Default: the shipped table's ``lookup`` row (the reference's rule, e.g.
+    cfg4 -> the P=15 N=2048 row, the largest stored).  ``optimal=True``:
+    the optimal schedule for the config's exact N from ``optimize`` (the
+    reference's ``optimize.solve``), e.g. P=15 at
+    N=32768 for cfg4.
+    """
     from .schedule import effective_n, quantize
     from .tables import shipped_table
 
@@ -58,6 +65,10 @@ def config_schedule(name, table=None):
     if n == "effective":
         shape = cfg["shape"]
         n = effective_n([s + 1 for s in shape], len(shape), "dirichlet")
+    if optimal:
+        from .optimize import optimal_schedule
+
+        return quantize(optimal_schedule(cfg["p"], int(n), table=table))
     return quantize(table.lookup(cfg["p"], int(n)))
 
 

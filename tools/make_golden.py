@@ -132,6 +132,29 @@ def bc_fixture(name, prob, weights, steps, tol=1e-300, post=None):
     save(name, **arr)
 
 
+def optimizer_fixtures(cases=((2, 300, "neumann", 2), (3, 90, "dirichlet", 3),
+                                 (4, 1000, "neumann", 2), (5, 333, "dirichlet", 2),
+                                 (6, 300, "neumann", 2), (6, 4096, "neumann", 2),
+                                 (8, 700, "neumann", 2), (10, 512, "neumann", 2),
+                                 (12, 3000, "neumann", 2), (13, 128, "neumann", 2))):
+    """Optimal schedules from the reference optimizer (optimize.solve,
+    optimize.py:803-879) for tabulated and untabulated (P, N)."""
+    import time
+
+    from srj import optimize as O
+
+    arr = {}
+    for p, n, bc, d in cases:
+        t0 = time.time()
+        rep = O.solve(p, n, bc=bc, d=d)
+        tag = f"p{p}_n{n}_{bc}_d{d}"
+        arr[tag + "_omegas"] = np.asarray(rep.schedule.omegas, dtype=float)
+        arr[tag + "_betas"] = np.asarray(rep.schedule.betas, dtype=float)
+        arr[tag + "_case"] = np.array([p, n, d, 1 if bc == "dirichlet" else 0])
+        print(tag, f"{time.time() - t0:.1f}s", flush=True)
+        save("optimizer", **arr)  # incremental: keep what finished
+
+
 def spherical_fixtures():
     """Spherical Poisson (problems.py:443-600): mask + mirror/periodic ghosts +
     the tie_origin post_sweep hook (u[1] = u[2], u[0] = u[2])."""
@@ -293,5 +316,7 @@ def main():
 if __name__ == "__main__":
     if sys.argv[1:] == ["spherical"]:
         spherical_fixtures()
+    elif sys.argv[1:] == ["optimizer"]:
+        optimizer_fixtures()
     else:
         main()
