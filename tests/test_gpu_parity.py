@@ -573,3 +573,55 @@ def test_post_sweep_gather_overlapping_vs_oracle(table):
     _, _, norms = oracle.run_bc(q, spec, w, 90, post=chain)
     assert np.array_equal(p.u, q.u)
     assert np.array_equal(hist.true_residual_inf, norms[:, 1])
+
+
+def test_capi_run_time_errors():
+    """srj_plan_run / srj_plan_set_post_gather argument errors (status codes +
+    srj_last_error), on a live plan."""
+    from paper_1511_04292_b200 import _lib
+    from paper_1511_04292_b200.engine import DeviceGrid
+
+    f = config_fields("cfg2", (40, 70))
+    g = DeviceGrid(f["u"], f["source"], f["center"], f["lower"], f["upper"])
+    lib, plan = g.lib, g.plan
+    fa, fb, fc = (ctypes.c_void_p(t.data_ptr()) for t in g.fields)
+    w = np.array([1.0, 0.5])
+    wp = w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    out = ctypes.c_int32(-1)
+    norms = ctypes.c_void_p(g.norms.data_ptr())
+
+    def run(src, a, b, m=2, first=0, n=1, fuse=0, nrm=norms):
+        return lib.srj_plan_run(plan, src, a, b, wp, m, first, n, fuse, nrm, ctypes.byref(out),
+                                g._sp)
+
+    assert run(fa, fa, fb) == _lib.SRJ_EINVAL and b"distinct" in lib.srj_last_error()
+    assert run(fa, fb, fc, m=0) == _lib.SRJ_EINVAL
+    assert run(fa, fb, fc, first=-1) == _lib.SRJ_EINVAL
+    assert run(fa, fb, fc, n=1, fuse=lib.srj_max_fuse() + 1) == _lib.SRJ_EINVAL
+    assert run(fa, fb, fc, n=1, nrm=None) == _lib.SRJ_EINVAL
+    assert run(fa, fb, fc, n=0) == _lib.SRJ_OK and out.value == 0
+    g.ensure_norms(4)
+    assert run(fa, fb, fc, n=4, nrm=ctypes.c_void_p(g.norms.data_ptr())) == _lib.SRJ_OK
+    assert out.value in (1, 2)
+    lay = g.layout
+    bad = np.array([int(lay.elems)], dtype=np.int64)
+    ok = np.array([5], dtype=np.int64)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    assert lib.srj_plan_set_post_gather(plan, ptr(bad), ptr(ok), 1) == _lib.SRJ_EINVAL
+    dup = np.array([5, 5], dtype=np.int64)
+    assert lib.srj_plan_set_post_gather(plan, ptr(dup), ptr(dup), 2) == _lib.SRJ_EINVAL
+    assert b"distinct" in lib.srj_last_error()
+    assert lib.srj_plan_set_post_gather(plan, None, None, 0) == _lib.SRJ_OK
+    g.close()
+
+    # a slab plan (exchanged faces): fused depth limited by its halo, and
+    # gathers need the whole grid
+    s = DeviceGrid(f["u"], f["source"], f["center"], f["lower"], f["upper"], halo0=2,
+                   own=(2, 38), physical=(False, False))
+    s.ensure_norms(4)
+    fa, fb, fc = (ctypes.c_void_p(t.data_ptr()) for t in s.fields)
+    rc = s.lib.srj_plan_run(s.plan, fa, fb, fc, wp, 2, 0, 4, 3, ctypes.c_void_p(s.norms.data_ptr()),
+                            ctypes.byref(out), s._sp)
+    assert rc == _lib.SRJ_EINVAL and b"halo0" in s.lib.srj_last_error()
+    assert s.lib.srj_plan_set_post_gather(s.plan, ptr(ok), ptr(ok + 1), 1) == _lib.SRJ_EUNSUPPORTED
+    s.close()
