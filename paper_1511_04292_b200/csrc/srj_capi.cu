@@ -223,8 +223,7 @@ Kernel3DTB pick3d_tb_t(bool nl, bool recip) {
 Kernel3DTB pick3d_tb(int T, bool nl, bool recip) {
   switch (T) {
     case 2: return pick3d_tb_t<2>(nl, recip);
-    case 3: return pick3d_tb_t<3>(nl, recip);
-    default: return pick3d_tb_t<4>(nl, recip);
+    default: return pick3d_tb_t<3>(nl, recip);
   }
 }
 
