@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -93,15 +94,45 @@ int bps_override() {
   return b;
 }
 
-int sm_count() {
-  static int n = 0;
+// Per-device caches: function attributes and occupancy belong to a device
+// context, so one process may drive several GPUs (from several threads).
+// Races only repeat idempotent work.
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & (kMaxDevices - 1);
+}
+
+// Runs f() once per device for the given cache of flags.
+template <typename F>
+void once_per_device(std::atomic<uint64_t> &done, F &&f) {
+  const uint64_t bit = uint64_t(1) << current_device();
+  if (done.load(std::memory_order_acquire) & bit) return;
+  f();
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
+
+// Per-device integer cache filled by f() (0 = not yet computed).
+template <typename F>
+int cached_per_device(std::atomic<int> (&slot)[kMaxDevices], F &&f) {
+  std::atomic<int> &v = slot[current_device()];
+  int n = v.load(std::memory_order_acquire);
   if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+    n = f();
+    v.store(n, std::memory_order_release);
   }
   return n;
+}
+
+int sm_count() {
+  static std::atomic<int> cache[kMaxDevices];
+  return cached_per_device(cache, [] {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device());
+    return n > 0 ? n : 148;
+  });
 }
 
 // ------------------------------------------------------------ 2D dispatch
@@ -121,12 +152,11 @@ struct K2 {
   static constexpr int V = 2;
   using B = Band2D<T, V>;
   static void configure() {
-    static bool done = false;
-    if (!done) {
+    static std::atomic<uint64_t> done{0};
+    once_per_device(done, [] {
       cudaFuncSetAttribute(sweep2d_tb<T, V, VAR, NL, RECIP>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(B::smem_bytes()));
-      done = true;
-    }
+    });
   }
   static void launch(const Sweep2DParams &p, const CUtensorMap &tu, const CUtensorMap &tf,
                      int blocks, cudaStream_t s) {
@@ -134,14 +164,14 @@ struct K2 {
     sweep2d_tb<T, V, VAR, NL, RECIP><<<blocks, B::WARPS * 32, B::smem_bytes(), s>>>(p, tu, tf);
   }
   static int bps() {
-    static int n = 0;
-    if (n == 0) {
+    static std::atomic<int> cache[kMaxDevices];
+    return cached_per_device(cache, [] {
       configure();
+      int n = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_tb<T, V, VAR, NL, RECIP>,
                                                     B::WARPS * 32, B::smem_bytes());
-      if (n <= 0) n = 1;
-    }
-    return n;
+      return n > 0 ? n : 1;
+    });
   }
   static Kernel2D get() { return Kernel2D{launch, B::BAND, bps, B::OWN}; }
 };
@@ -165,12 +195,12 @@ struct K3 {
     sweep3d<VAR, NL, RECIP><<<blocks, kWarps3D * 32, 0, s>>>(p);
   }
   static int bps() {
-    static int n = 0;
-    if (n == 0) {
+    static std::atomic<int> cache[kMaxDevices];
+    return cached_per_device(cache, [] {
+      int n = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d<VAR, NL, RECIP>, kWarps3D * 32, 0);
-      if (n <= 0) n = 1;
-    }
-    return n;
+      return n > 0 ? n : 1;
+    });
   }
   static Kernel3D get() { return Kernel3D{launch, bps}; }
 };
@@ -189,12 +219,11 @@ template <int T, bool NL, bool RECIP>
 struct K3TB {
   using B = Tile3D<T>;
   static void configure() {
-    static bool done = false;
-    if (!done) {
+    static std::atomic<uint64_t> done{0};
+    once_per_device(done, [] {
       cudaFuncSetAttribute(sweep3d_tb<T, NL, RECIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(B::smem_bytes()));
-      done = true;
-    }
+    });
   }
   static void launch(const Sweep3DTBParams &p, const CUtensorMap &tu, const CUtensorMap &tf,
                      int blocks, cudaStream_t s) {
@@ -202,14 +231,14 @@ struct K3TB {
     sweep3d_tb<T, NL, RECIP><<<blocks, B::THREADS, B::smem_bytes(), s>>>(p, tu, tf);
   }
   static int bps() {
-    static int n = 0;
-    if (n == 0) {
+    static std::atomic<int> cache[kMaxDevices];
+    return cached_per_device(cache, [] {
       configure();
+      int n = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d_tb<T, NL, RECIP>, B::THREADS,
                                                     B::smem_bytes());
-      if (n <= 0) n = 1;
-    }
-    return n;
+      return n > 0 ? n : 1;
+    });
   }
   static Kernel3DTB get() { return Kernel3DTB{launch, bps, B::TJ, B::TK, B::HS, B::HJ}; }
 };
@@ -578,13 +607,12 @@ static bool cluster_fits(const srj_plan &plan, int &C, int &R) {
 
 template <bool VAR, bool NL, bool RECIP>
 static int launch_cluster(const Cluster2DParams &p, int C, size_t smem, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  once_per_device(configured, [] {
     cudaFuncSetAttribute(sweep2d_cluster<VAR, NL, RECIP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(sweep2d_cluster<VAR, NL, RECIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    configured = true;
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, 1, 1);
   cfg.blockDim = dim3(kClusterThreads, 1, 1);

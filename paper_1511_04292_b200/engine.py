@@ -186,6 +186,10 @@ class DeviceGrid:
         self.stream.synchronize()  # host array may be a temporary
 
     def upload_field(self, host, dev):
+        with self._on():
+            self._upload_field(host, dev)
+
+    def _upload_field(self, host, dev):
         _lib.check(self.lib.srj_upload_field(
             ctypes.byref(self.layout), host.ctypes.data_as(ctypes.c_void_p),
             ctypes.c_void_p(dev.data_ptr()), self._sp), "srj_upload_field")
@@ -198,9 +202,10 @@ class DeviceGrid:
             self.download_field(idx, tmp)
             host[...] = tmp
             return
-        _lib.check(self.lib.srj_download_field(
-            ctypes.byref(self.layout), ctypes.c_void_p(self.fields[idx].data_ptr()),
-            host.ctypes.data_as(ctypes.c_void_p), self._sp), "srj_download_field")
+        with self._on():
+            _lib.check(self.lib.srj_download_field(
+                ctypes.byref(self.layout), ctypes.c_void_p(self.fields[idx].data_ptr()),
+                host.ctypes.data_as(ctypes.c_void_p), self._sp), "srj_download_field")
         self.stream.synchronize()
 
     # -------------------------------------------------------------- compute
@@ -208,6 +213,10 @@ class DeviceGrid:
         if self.norms.numel() < 2 * nsteps:
             self.norms = self.torch.zeros(2 * nsteps, dtype=self.torch.float64,
                                           device=self.device)
+
+    def _on(self):
+        """The library launches on the current CUDA device: make it ours."""
+        return self.torch.cuda.device(self.device)
 
     def run(self, src, weights, first, nsteps, fuse=0):
         """Run steps [first, first+nsteps) from buffer ``src``; returns the
@@ -217,25 +226,28 @@ class DeviceGrid:
         w = np.ascontiguousarray(weights, dtype=np.float64)
         out = ctypes.c_int32(0)
         f = self.fields
-        _lib.check(self.lib.srj_plan_run(
-            self.plan, ctypes.c_void_p(f[src].data_ptr()),
-            ctypes.c_void_p(f[a].data_ptr()), ctypes.c_void_p(f[b].data_ptr()),
-            w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(w), int(first),
-            int(nsteps), int(fuse), ctypes.c_void_p(self.norms.data_ptr()),
-            ctypes.byref(out), self._sp), "srj_plan_run")
+        with self._on():
+            _lib.check(self.lib.srj_plan_run(
+                self.plan, ctypes.c_void_p(f[src].data_ptr()),
+                ctypes.c_void_p(f[a].data_ptr()), ctypes.c_void_p(f[b].data_ptr()),
+                w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(w), int(first),
+                int(nsteps), int(fuse), ctypes.c_void_p(self.norms.data_ptr()),
+                ctypes.byref(out), self._sp), "srj_plan_run")
         return (src, a, b)[out.value]
 
     def residual(self, idx):
         """(sum r^2, max|r|) of field buffer ``idx`` (synchronous)."""
-        _lib.check(self.lib.srj_plan_residual(
-            self.plan, ctypes.c_void_p(self.fields[idx].data_ptr()),
-            ctypes.c_void_p(self.resid_out.data_ptr()), self._sp), "srj_plan_residual")
+        with self._on():
+            _lib.check(self.lib.srj_plan_residual(
+                self.plan, ctypes.c_void_p(self.fields[idx].data_ptr()),
+                ctypes.c_void_p(self.resid_out.data_ptr()), self._sp), "srj_plan_residual")
         v = self.resid_out.cpu().numpy()
         return float(v[0]), float(v[1])
 
     def close(self):
         if getattr(self, "plan", None) is not None:
-            self.lib.srj_plan_destroy(self.plan)
+            with self._on():
+                self.lib.srj_plan_destroy(self.plan)
             self.plan = None
 
     def __del__(self):
