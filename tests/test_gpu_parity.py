@@ -625,3 +625,18 @@ def test_capi_run_time_errors():
     assert rc == _lib.SRJ_EINVAL and b"halo0" in s.lib.srj_last_error()
     assert s.lib.srj_plan_set_post_gather(s.plan, ptr(ok), ptr(ok + 1), 1) == _lib.SRJ_EUNSUPPORTED
     s.close()
+
+
+def test_c_abi_demo_program():
+    """examples/srj_c_demo.c drives the C ABI from plain C (no Python, no
+    torch): plan API and dense kernel entry point vs a CPU loop, bitwise."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples",
+                       "bin", "srj_c_demo")
+    if not os.path.exists(exe):
+        pytest.skip("examples/bin/srj_c_demo not built (run __graft_entry__.build())")
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "OK" in res.stdout and "mismatches 0, dense mismatches 0, norms equal" in res.stdout
