@@ -87,7 +87,7 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, const double (&u
                                         const double (&mid)[V], const double (&down)[V],
                                         const double *frow, int r, double om, int lane_col,
                                         int i0, int i1, int own_c0, int own_c1, int f_lo,
-                                        int f_hi, unsigned colact, double (&y)[V],
+                                        int f_hi, unsigned colact, bool cnt, double (&y)[V],
                                         double (&num)[V], double &rmx, double &dmx, bool &bad) {
   double fv[V];
 #pragma unroll
@@ -136,9 +136,9 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, const double (&u
     cv[v] = c;
     actv[v] = act;
     if (FAST && !EDGE) {
-      acc_absmax(rmx, rr);  // garbage lanes are excluded at the warp vote
+      if (cnt) acc_absmax(rmx, rr);  // garbage lanes are excluded at the warp vote
     } else if (FAST) {
-      if ((colact >> (V + v)) & 1u) acc_absmax(rmx, rr);  // owned-column bit
+      if (cnt && ((colact >> (V + v)) & 1u)) acc_absmax(rmx, rr);  // owned-column bit
     } else if (act && row_own && col >= own_c0 && col < own_c1) {
       acc_absmax(rmx, rr);
     }
@@ -239,9 +239,11 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
   const int f_lo = p.lo_c, f_hi = p.hi_c - 1;
   const bool band_interior = (col_band >= 0) && (col_band + BAND <= p.n1) && !VAR;
   const bool band_edge = !band_interior && !VAR;  // fast rows, masked columns
-  // fast ticks: every stage row rho-2t (t=1..T) owned and relaxing
-  const int fast_lo = max(i0, p.lo_c) + 2 * T;
-  const int fast_hi = min(i1, p.hi_c) + 1;
+  // fast ticks: every stage row rho-2t (t=1..T) relaxes (rows outside the
+  // strip -- its dependency halo and the pipeline fill/drain -- are computed
+  // the same way; only the owned ones count in the norms, flag cnt)
+  const int fast_lo = p.lo_c + 2 * T;
+  const int fast_hi = p.hi_c + 1;
   const int lane_col = col_band + V * lane;
   const bool lane_owned = (lane_col >= own_c0) && (lane_col + V <= own_c1);
   // bit v: column lane_col+v is interior (relaxes); bit V+v: it is owned
@@ -309,7 +311,8 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
     stage2d<FASTV, EDGEV, VAR, NL, RECIP, V>(p, w[t][ph % 3], w[t][(ph + 1) % 3],            \
                                       w[t][(ph + 2) % 3], frow, rho - 2 * t, p.omega[t - 1],  \
                                       lane_col, i0, i1, own_c0, own_c1, f_lo, f_hi, colact,   \
-                                      dst, num[t], rmx[t - 1], dmx[t - 1], bad);              \
+                                      rho - 2 * t >= i0 && rho - 2 * t < i1, dst, num[t],     \
+                                      rmx[t - 1], dmx[t - 1], bad);                           \
   }                                                                                           \
   if (RECIP && __any_sync(kFull, bad)) {                                                      \
     _Pragma("unroll") for (int t = T; t >= 1; --t) {                                          \
