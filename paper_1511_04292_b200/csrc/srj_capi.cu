@@ -21,6 +21,7 @@
 #include "srj_sweep2d.cuh"
 #include "srj_sweep3d.cuh"
 #include "srj_cluster2d.cuh"
+#include "srj_sweep2d_var.cuh"
 #include "srj_sweep3d_tb.cuh"
 
 using namespace srj;
@@ -204,6 +205,72 @@ struct K3 {
   }
   static Kernel3D get() { return Kernel3D{launch, bps}; }
 };
+
+// 2D per-cell coefficients, one sweep (HBM-bound streaming kernel)
+template <bool NL>
+struct KVar2D {
+  static int bps() {
+    static std::atomic<int> cache[kMaxDevices];
+    return cached_per_device(cache, [] {
+      int n = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_var<NL>, kWarps2DVar * 32, 0);
+      return n > 0 ? n : 1;
+    });
+  }
+};
+
+static int launch_var2d(const srj_plan_desc &d, const double *cur, double *nxt, const double *f,
+                        int ld_lo, int ld_hi, double omega, double *norms, cudaStream_t st) {
+  const srj_layout_t &l = d.layout;
+  const int64_t ioff = interior_offset(l);
+  const bool nl = d.kappa != nullptr;
+  Var2DParams p{};
+  p.src = cur + ioff;
+  p.dst = nxt + ioff;
+  p.f = f + ioff;
+  p.act = d.act ? d.act + ioff : nullptr;
+  p.c = d.coef_arrays[0] + ioff;
+  p.am0 = d.coef_arrays[1] + ioff;
+  p.ap0 = d.coef_arrays[2] + ioff;
+  p.am1 = d.coef_arrays[3] + ioff;
+  p.ap1 = d.coef_arrays[4] + ioff;
+  p.pitch = l.pitch;
+  p.n0 = int(l.n[0]);
+  p.n1 = int(l.n[1]);
+  p.ld_lo = ld_lo;
+  p.ld_hi = ld_hi;
+  p.own_b = int(d.own0_begin);
+  p.own_e = int(d.own0_end);
+  p.nbands = int((l.n[1] + 63) / 64);
+  p.omega = omega;
+  p.norms = norms;
+  const int rows = p.own_e - p.own_b;
+  const long capacity = long(sm_count()) * (nl ? KVar2D<true>::bps() : KVar2D<false>::bps()) *
+                        kWarps2DVar;
+  // strips: best fill of whole waves, discounting the 2 halo rows per strip
+  int nstrips = 1;
+  double best = -1.0;
+  for (int ns = 1; ns <= std::max(1, std::min(256, rows / 8)); ++ns) {
+    const long w = long(p.nbands) * ns;
+    const long waves = (w + capacity - 1) / capacity;
+    const double hh = double(rows) / ns;
+    const double eff = double(w) / double(waves * capacity) * hh / (hh + 2.0);
+    if (eff > best + 1e-9) {
+      best = eff;
+      nstrips = ns;
+    }
+  }
+  p.H = (rows + nstrips - 1) / nstrips;
+  p.nstrips = (rows + p.H - 1) / p.H;
+  const long warps = long(p.nbands) * p.nstrips;
+  const int blocks = int((warps + kWarps2DVar - 1) / kWarps2DVar);
+  if (nl)
+    sweep2d_var<true><<<blocks, kWarps2DVar * 32, 0, st>>>(p);
+  else
+    sweep2d_var<false><<<blocks, kWarps2DVar * 32, 0, st>>>(p);
+  SRJ_CUDA(cudaGetLastError());
+  return SRJ_OK;
+}
 
 // temporally blocked 3D (constant stencil only)
 constexpr int kMaxFuse3D = 3;  // T=4 tiles exceed shared memory
@@ -745,7 +812,11 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
   int64_t k = 0;
   while (k < nsteps) {
     const int t = int(std::min<int64_t>(T, nsteps - k));
-    if (l.ndim == 2) {
+    if (l.ndim == 2 && var && t == 1) {
+      const int rc = launch_var2d(d, cur, nxt, f, ld_lo, ld_hi, weights[(first + k) % m],
+                                  d_norms + 2 * k, st);
+      if (rc != SRJ_OK) return rc;
+    } else if (l.ndim == 2) {
       Sweep2DParams p{};
       p.src = cur + ioff;
       p.dst = nxt + ioff;

@@ -640,3 +640,23 @@ def test_c_abi_demo_program():
     res = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "OK" in res.stdout and "mismatches 0, dense mismatches 0, norms equal" in res.stdout
+
+
+@pytest.mark.parametrize("masked", [False, True])
+def test_per_cell_coefficients_2d_streaming_kernel(masked):
+    """2D per-cell coefficients above the small-grid cluster size run the
+    streaming single-sweep kernel (srj_sweep2d_var.cuh): bitwise vs oracle,
+    ragged width, mask with inactive cells that must keep their value."""
+    rng = np.random.default_rng(7)
+    shape = (700, 611)
+    f = {"u": rng.standard_normal((702, 613)), "source": rng.standard_normal(shape),
+         "center": 4.0 + rng.random(shape),
+         "lower": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(2)),
+         "upper": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(2)),
+         "mask": (rng.random(shape) > 0.1) if masked else None}
+    w = np.array([1.6, 0.6, 1.1])
+    want, norms = oracle_steps(f, w, 45)
+    p = problem_from(f)
+    hist, _ = run_steps(p, w, 45, fuse=1, chunk=20)
+    assert np.array_equal(p.u, want.u)
+    assert np.array_equal(hist.true_residual_inf, norms[:, 1])
