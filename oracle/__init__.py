@@ -11,6 +11,8 @@ running the reference's own ``srj_solve`` / ``weighted_jacobi_sweep`` here.
 
 from .oracle import (  # noqa: F401
     OVERFLOW_LIMIT,
+    gs_solve,
+    gs_sweep,
     load,
     np_step,
     refresh_ghosts,

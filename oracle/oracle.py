@@ -60,6 +60,11 @@ def load():
         ctypes.POINTER(_dp), ctypes.POINTER(_dp), _u8p, ctypes.c_double,
         _dp, _dp, ctypes.c_int,
     ]
+    lib.oracle_gs.restype = ctypes.c_int
+    lib.oracle_gs.argtypes = [
+        ctypes.c_int, _i64p, _dp, _dp, _dp, ctypes.POINTER(_dp), ctypes.POINTER(_dp), _u8p,
+        ctypes.c_double, _dp, _dp,
+    ]
     lib.oracle_run.restype = ctypes.c_int64
     lib.oracle_run.argtypes = [
         ctypes.c_int, _i64p, _dp, _dp, _dp, _dp,
@@ -312,3 +317,41 @@ def run_bc(problem, bc, weights, nsteps, tol=0.0, kappa=None, post=None):
                 status = 1
                 break
     return len(norms), status, np.asarray(norms).reshape(-1, 2)
+
+
+def gs_sweep(problem, omega):
+    """One in-place lexicographic Gauss-Seidel / SOR sweep (``_gs2``/``_gs3``,
+    grids.py:426-474); returns (dmax, rmax).  Ghosts are not refreshed."""
+    lib = load()
+    a = _Args(problem)
+    u = _field(problem)
+    dm, rm = ctypes.c_double(), ctypes.c_double()
+    rc = lib.oracle_gs(a.ndim, _ptr(a.n, _i64p), _ptr(u), _ptr(a.s), _ptr(a.c), a.lo_p, a.hi_p,
+                       _ptr(a.act, _u8p), float(omega), ctypes.byref(dm), ctypes.byref(rm))
+    if rc != 0:
+        raise ValueError("oracle GS supports 2- and 3-dimensional grids")
+    return dm.value, rm.value
+
+
+def gs_solve(problem, omega, nsteps, tol=0.0, bc=None, sor=False):
+    """``gauss_seidel_solve`` (omega = 1) / ``sor_solve`` (grids.py:697-716): the
+    reference loop ``_iterate`` (:602-629) over GS sweeps with the ghost refresh
+    of ``_Sweeper.gauss_seidel`` (:561-571); the SOR metric is dmax/omega.
+    Returns (steps, status, norms[steps, 2] = (metric, rmax))."""
+    norms = []
+    status = 0
+    for _ in range(int(nsteps)):
+        dm, rm = gs_sweep(problem, omega)
+        if bc is not None:
+            refresh_ghosts(problem.u, bc)
+        metric = dm / omega if sor else dm
+        norms.append((metric, rm))
+        if tol != 0.0:
+            if not np.isfinite(metric) or metric > OVERFLOW_LIMIT:
+                status = 2
+                break
+            if tol > 0.0 and metric < tol:
+                status = 1
+                break
+    return len(norms), status, np.asarray(norms).reshape(-1, 2)
+

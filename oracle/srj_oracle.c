@@ -9,6 +9,8 @@
  * What it restates (reference = /root/reference/pkg/src/srj/grids.py):
  *   oracle_wj1/2/3   <- _wj1 (grids.py:331-348), _wj2 (:351-376), _wj3 (:379-408)
  *   oracle_solve     <- _iterate (:602-629) driven as srj_solve (:642-687)
+ *   oracle_gs        <- _gs2 (grids.py:426-448), _gs3 (:450-474): in-place
+ *                       lexicographic Gauss-Seidel / SOR sweeps
  *   oracle_residual  <- GridProblem.residual_field (:249-266), reduced to
  *                       (sum r^2, max |r|) -- the L2 norm is this project's
  *                       addition (BASELINE north_star), not in the reference.
@@ -179,6 +181,59 @@ int oracle_wj(int ndim, const int64_t *n, const double *u, double *un,
                 if (lrm > rm) rm = lrm;
             }
         }
+    } else {
+        return -1;
+    }
+    *dmax = dm;
+    *rmax = rm;
+    return 0;
+}
+
+/* One in-place lexicographic Gauss-Seidel/SOR sweep (_gs2 / _gs3): each cell
+ * uses the already-updated values of its lower neighbours along every axis
+ * and the old values of its upper neighbours.  Sequential by definition. */
+int oracle_gs(int ndim, const int64_t *n, double *u, const double *s,
+              const double *c, const double *const *lower,
+              const double *const *upper, const uint8_t *act, double omega,
+              double *dmax, double *rmax) {
+    double dm = 0.0, rm = 0.0;
+    if (ndim == 2) {
+        const int64_t n0 = n[0], n1 = n[1], w = n1 + 2;
+        for (int64_t i = 0; i < n0; ++i)
+            for (int64_t j = 0; j < n1; ++j) {
+                const int64_t q = i * n1 + j;
+                if (act && !act[q]) continue;
+                const int64_t g = (i + 1) * w + (j + 1);
+                const double uc = u[g];
+                const double acc = c[q] * uc + lower[0][q] * u[g - w] +
+                                   upper[0][q] * u[g + w] + lower[1][q] * u[g - 1] +
+                                   upper[1][q] * u[g + 1];
+                const double r = s[q] - acc;
+                const double d = omega * r / c[q];
+                u[g] = uc + d;
+                upd_max(&dm, d);
+                upd_max(&rm, r);
+            }
+    } else if (ndim == 3) {
+        const int64_t n0 = n[0], n1 = n[1], n2 = n[2];
+        const int64_t w = n2 + 2, pl = (n1 + 2) * w;
+        for (int64_t i = 0; i < n0; ++i)
+            for (int64_t j = 0; j < n1; ++j)
+                for (int64_t k = 0; k < n2; ++k) {
+                    const int64_t q = (i * n1 + j) * n2 + k;
+                    if (act && !act[q]) continue;
+                    const int64_t g = (i + 1) * pl + (j + 1) * w + (k + 1);
+                    const double uc = u[g];
+                    const double acc = c[q] * uc + lower[0][q] * u[g - pl] +
+                                       upper[0][q] * u[g + pl] + lower[1][q] * u[g - w] +
+                                       upper[1][q] * u[g + w] + lower[2][q] * u[g - 1] +
+                                       upper[2][q] * u[g + 1];
+                    const double r = s[q] - acc;
+                    const double d = omega * r / c[q];
+                    u[g] = uc + d;
+                    upd_max(&dm, d);
+                    upd_max(&rm, r);
+                }
     } else {
         return -1;
     }

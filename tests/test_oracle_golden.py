@@ -153,3 +153,24 @@ def test_dependency_cone_crops(name, shape, k):
         b = q.u[tuple(slice(s.start + 1, s.stop + 1) for s in win)]
         assert np.array_equal(a, b) == same
     assert nd == len(win)
+
+
+GS_CASES = ["gs_var2d", "sor_var2d", "gs_var3d", "sor_var3d", "gs_const2d_solve", "sor_neumann2d"]
+
+
+@pytest.mark.parametrize("name", GS_CASES)
+def test_oracle_gauss_seidel_matches_reference(name):
+    """oracle_gs (lexicographic in-place sweeps) reproduces the reference
+    gauss_seidel_solve / sor_solve bit for bit (fields, both histories,
+    iteration count of the tolerance run)."""
+    from conftest import bc_from
+
+    g = load_golden(name)
+    p = problem_from(fields_from(g))
+    steps, status, norms = oracle.gs_solve(p, float(g["omega"]), int(g["steps"]),
+                                           tol=float(g["tol"]), bc=bc_from(g), sor=bool(g["sor"]))
+    assert steps == len(g["residual_inf"])
+    assert status == (1 if bool(g["converged"]) else 0)
+    assert np.array_equal(p.u, g["u_final"])
+    assert np.array_equal(norms[:, 0], g["residual_inf"])
+    assert np.array_equal(norms[:, 1], g["true_residual_inf"])

@@ -155,6 +155,45 @@ def optimizer_fixtures(cases=((2, 300, "neumann", 2), (3, 90, "dirichlet", 3),
         save("optimizer", **arr)  # incremental: keep what finished
 
 
+def gs_fixtures():
+    """Gauss-Seidel / SOR (grids.py:410-476, :697-716): in-place lexicographic
+    sweeps, reference ghost refresh after each, fixed-step and tolerance runs."""
+    from srj.problems import laplace2d_neumann
+
+    rng = np.random.default_rng(1511)
+
+    def run(name, prob, omega, steps, tol=1e-300):
+        nd = prob.ndim
+        arr = {"u0": prob.u.copy(), "source": prob.source.copy(), "center": prob.center.copy()}
+        for ax in range(nd):
+            arr[f"lower{ax}"] = prob.lower[ax].copy()
+            arr[f"upper{ax}"] = prob.upper[ax].copy()
+            for side in range(2):
+                arr[f"bc{ax}{side}"] = np.array(prob.bc[ax][side].kind)
+        if prob.mask is not None:
+            arr["mask"] = prob.mask.copy()
+        if omega is None:
+            hist, _ = G.gauss_seidel_solve(prob, tol=tol, max_iters=steps)
+        else:
+            hist, _ = G.sor_solve(prob, omega, tol=tol, max_iters=steps)
+        arr.update(omega=np.float64(1.0 if omega is None else omega), sor=np.bool_(omega is not None),
+                   steps=np.int64(steps), tol=np.float64(tol), u_final=prob.u,
+                   residual_inf=hist.residual_inf, true_residual_inf=hist.true_residual_inf,
+                   converged=np.bool_(hist.converged))
+        save(name, **arr)
+
+    run("gs_var2d", ref_problem(random_fields(rng, (37, 45), True)), None, 60)
+    run("sor_var2d", ref_problem(random_fields(rng, (70, 33), False)), 1.6, 60)
+    run("gs_var3d", ref_problem(random_fields(rng, (9, 14, 10), True)), None, 40)
+    run("sor_var3d", ref_problem(random_fields(rng, (12, 11, 13), False)), 1.3, 40)
+    c2 = P.poisson_fields((40, 52), n_gauss=8, seed=1, noise=False, width=(0.02, 0.1))
+    run("gs_const2d_solve", ref_problem(c2), None, 20000, tol=1e-9)
+    nm = laplace2d_neumann(24)
+    nm.u[1:-1, 1:-1] = np.random.default_rng(3).standard_normal(nm.shape)
+    nm.refresh_ghosts()
+    run("sor_neumann2d", nm, 1.7, 80)
+
+
 def spherical_fixtures():
     """Spherical Poisson (problems.py:443-600): mask + mirror/periodic ghosts +
     the tie_origin post_sweep hook (u[1] = u[2], u[0] = u[2])."""
@@ -274,6 +313,7 @@ def main():
     bc_fixture("facedir3d", fd, w64, 120)
 
     spherical_fixtures()
+    gs_fixtures()
     bc_fixture("gs_a", grad_shafranov("A", 0.0, 40), w64, 300)
     bc_fixture("gs_b", grad_shafranov("B", 0.0, 48), w64, 300)
     gs_row = table.lookup(14, 300)
@@ -318,5 +358,7 @@ if __name__ == "__main__":
         spherical_fixtures()
     elif sys.argv[1:] == ["optimizer"]:
         optimizer_fixtures()
+    elif sys.argv[1:] == ["gs"]:
+        gs_fixtures()
     else:
         main()
