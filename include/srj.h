@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SRJ_ABI_VERSION 3
+#define SRJ_ABI_VERSION 4
 
 enum {
     SRJ_OK = 0,
@@ -172,6 +172,16 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a,
  * two-pass reduction (fixed order).  d_out: device, 2 doubles. */
 int srj_plan_residual(srj_plan *plan, const double *u, double *d_out,
                       void *stream);
+
+/* Gauss-Seidel / SOR: `nsweeps` in-place lexicographic sweeps of field `u`
+ * (a buffer in the plan's layout) with relaxation factor omega (1 = GS),
+ * bitwise the reference's _gs2 / _gs3 (grids.py:426-474) followed by its ghost
+ * refresh (and copy hook) after every sweep (_Sweeper.gauss_seidel,
+ * grids.py:561-571).  d_norms (device, 2*nsweeps doubles): per-sweep (dmax,
+ * rmax).  A GPU wavefront: 32-row strips must all be co-resident (cooperative
+ * launch), else SRJ_EUNSUPPORTED; whole-grid plans, no nonlinear source. */
+int srj_plan_gs(srj_plan *plan, double *u, double omega, int64_t nsweeps,
+                double *d_norms, void *stream);
 
 /* Host <-> device transfers between the reference's dense layout and the
  * padded layout (cudaMemcpy2DAsync; host memory should be pinned).

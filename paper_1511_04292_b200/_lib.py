@@ -17,7 +17,7 @@ SRJ_EINVAL = -1
 SRJ_ECUDA = -2
 SRJ_ENOMEM = -3
 SRJ_EUNSUPPORTED = -4
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 BC_KINDS = {"fixed": 0, "mirror": 1, "periodic": 2, "face_dirichlet": 3}
 
@@ -86,6 +86,8 @@ _SIGNATURES = {
                                     ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p]),
     "srj_plan_residual": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p]),
+    "srj_plan_gs": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                   ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "srj_upload_field": (ctypes.c_int, [ctypes.POINTER(SrjLayout), ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_void_p]),
     "srj_download_field": (ctypes.c_int, [ctypes.POINTER(SrjLayout), ctypes.c_void_p,

@@ -21,6 +21,7 @@
 #include "srj_sweep2d.cuh"
 #include "srj_sweep3d.cuh"
 #include "srj_cluster2d.cuh"
+#include "srj_gs.cuh"
 #include "srj_sweep2d_var.cuh"
 #include "srj_sweep3d_tb.cuh"
 
@@ -272,6 +273,38 @@ static int launch_var2d(const srj_plan_desc &d, const double *cur, double *nxt, 
   return SRJ_OK;
 }
 
+// Gauss-Seidel / SOR wavefront (srj_gs.cuh): nsweeps in-place sweeps, one
+// cooperative launch (every strip co-resident)
+template <int ND, bool VAR, bool RECIP>
+static int launch_gs_t(const GSParams &p, int nstrips, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nstrips);
+  cfg.blockDim = dim3(32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, gs_sweep<ND, VAR, RECIP>, p);
+  if (e == cudaErrorCooperativeLaunchTooLarge)
+    return fail(SRJ_EUNSUPPORTED, "Gauss-Seidel wavefront needs %d co-resident strips of 32 rows; "
+                "the grid has too many rows for one GPU", nstrips);
+  SRJ_CUDA(e);
+  return SRJ_OK;
+}
+
+static int launch_gs(const GSParams &p, int nd, bool var, bool recip, int nstrips, cudaStream_t st) {
+  if (nd == 2) {
+    if (var) return launch_gs_t<2, true, false>(p, nstrips, st);
+    return recip ? launch_gs_t<2, false, true>(p, nstrips, st)
+                 : launch_gs_t<2, false, false>(p, nstrips, st);
+  }
+  if (var) return launch_gs_t<3, true, false>(p, nstrips, st);
+  return recip ? launch_gs_t<3, false, true>(p, nstrips, st)
+               : launch_gs_t<3, false, false>(p, nstrips, st);
+}
+
 // temporally blocked 3D (constant stencil only)
 constexpr int kMaxFuse3D = 3;  // T=4 tiles exceed shared memory
 
@@ -400,6 +433,9 @@ struct srj_plan {
   double *d_omegas = nullptr, *h_omegas = nullptr;
   int64_t omega_cap = 0;
   cudaEvent_t omega_ev = nullptr;
+  // Gauss-Seidel wavefront progress counters (one per 32-row strip)
+  unsigned long long *gs_prog = nullptr;
+  int64_t gs_prog_cap = 0;
   // post-sweep gather (device copies; tmp only when dst and src overlap)
   int64_t *g_dst = nullptr, *g_src = nullptr;
   double *g_tmp = nullptr;
@@ -586,6 +622,7 @@ int srj_plan_set_post_gather(srj_plan *p, const int64_t *dst, const int64_t *src
 int srj_plan_destroy(srj_plan *p) {
   if (!p) return SRJ_OK;
   free_gather(p);
+  if (p->gs_prog) cudaFree(p->gs_prog);
   if (p->partials) cudaFree(p->partials);
   if (p->d_omegas) cudaFree(p->d_omegas);
   if (p->h_omegas) cudaFreeHost(p->h_omegas);
@@ -1014,6 +1051,71 @@ int srj_plan_residual(srj_plan *plan, const double *u, double *d_out, void *stre
        : residual_partial<false, false><<<kResidBlocks, kResidThreads, 0, st>>>(p);
   residual_final<<<1, 32, 0, st>>>(plan->partials, kResidBlocks, d_out);
   SRJ_CUDA(cudaGetLastError());
+  return SRJ_OK;
+}
+
+int srj_plan_gs(srj_plan *plan, double *u, double omega, int64_t nsweeps, double *d_norms,
+                void *stream) {
+  if (!plan || !u || (nsweeps > 0 && !d_norms)) return fail(SRJ_EINVAL, "null argument");
+  if (nsweeps < 0) return fail(SRJ_EINVAL, "negative sweep count");
+  if (nsweeps == 0) return SRJ_OK;
+  const srj_plan_desc &d = plan->d;
+  const srj_layout_t &l = d.layout;
+  if (d.kappa) return fail(SRJ_EUNSUPPORTED, "Gauss-Seidel has no nonlinear source");
+  if (!d.physical_lo0 || !d.physical_hi0 || d.own0_begin != 0 || d.own0_end != l.n[0])
+    return fail(SRJ_EUNSUPPORTED, "Gauss-Seidel needs the whole grid on one plan");
+  if (l.ndim == 3 && l.n[1] < 2)
+    return fail(SRJ_EUNSUPPORTED, "3-D Gauss-Seidel needs n[1] >= 2");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t ioff = interior_offset(l);
+  const bool var = d.coef_mode == 1;
+  GSParams p{};
+  p.u = u + ioff;
+  p.f = d.source + ioff;
+  p.act = d.act ? d.act + ioff : nullptr;
+  for (int a = 0; a < 7; ++a) {
+    p.coef[a] = (var && a < 1 + 2 * l.ndim) ? d.coef_arrays[a] + ioff : nullptr;
+    p.kc[a] = d.coef[a];
+  }
+  p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
+  p.kinv_lo = recip_lo(d.coef[0], p.kinv);
+  p.pitch = l.pitch;
+  p.plane = l.plane;
+  p.n1 = l.ndim == 3 ? int(l.n[1]) : 0;
+  p.nrows = l.ndim == 3 ? l.n[0] * l.n[1] : l.n[0];
+  p.ncols = int(l.n[l.ndim - 1]);
+  const int nstrips = int((p.nrows + 31) / 32);
+  p.nstrips = nstrips;
+  p.omega = omega;
+  if (nstrips > plan->gs_prog_cap) {
+    if (plan->gs_prog) cudaFree(plan->gs_prog);  // implicit device sync
+    plan->gs_prog = nullptr;
+    plan->gs_prog_cap = 0;
+    SRJ_CUDA(cudaMalloc(&plan->gs_prog, sizeof(unsigned long long) * size_t(nstrips)));
+    plan->gs_prog_cap = nstrips;
+  }
+  p.prog = plan->gs_prog;
+  SRJ_CUDA(cudaMemsetAsync(d_norms, 0, sizeof(double) * 2 * size_t(nsweeps), st));
+  const bool recip = !var && p.kinv != 0.0;
+  // non-FIXED faces / copy hooks: the reference refreshes ghosts after every
+  // sweep (_Sweeper.gauss_seidel, grids.py:561-571) -> one sweep per launch
+  const bool per_sweep = plan->has_bc || plan->g_n > 0;
+  const int64_t chunk = per_sweep ? 1 : (int64_t(1) << 20);
+  for (int64_t k = 0; k < nsweeps; k += chunk) {
+    p.nsweeps = int(std::min<int64_t>(chunk, nsweeps - k));
+    p.norms = d_norms + 2 * k;
+    SRJ_CUDA(cudaMemsetAsync(plan->gs_prog, 0, sizeof(unsigned long long) * size_t(nstrips), st));
+    const int rc = launch_gs(p, l.ndim, var, recip, nstrips, st);
+    if (rc != SRJ_OK) return rc;
+    if (plan->has_bc) {
+      const int rg = launch_ghosts(d, u + ioff, st);
+      if (rg != SRJ_OK) return rg;
+    }
+    if (plan->g_n > 0) {
+      const int rg = launch_gather(*plan, u, st);
+      if (rg != SRJ_OK) return rg;
+    }
+  }
   return SRJ_OK;
 }
 

@@ -235,6 +235,20 @@ class DeviceGrid:
                 ctypes.byref(out), self._sp), "srj_plan_run")
         return (src, a, b)[out.value]
 
+    def gs(self, idx, omega, nsweeps):
+        """``nsweeps`` in-place Gauss-Seidel / SOR sweeps of field buffer
+        ``idx`` (srj_plan_gs); per-sweep (dmax, rmax) land in ``self.norms``."""
+        self.ensure_norms(max(nsweeps, 1))
+        with self._on():
+            _lib.check(self.lib.srj_plan_gs(
+                self.plan, ctypes.c_void_p(self.fields[idx].data_ptr()), float(omega),
+                int(nsweeps), ctypes.c_void_p(self.norms.data_ptr()), self._sp), "srj_plan_gs")
+
+    def copy_field(self, src, dst):
+        """Device copy of field buffer ``src`` into ``dst`` (stream-ordered)."""
+        with self._on(), self.torch.cuda.stream(self.stream):
+            self.fields[dst].copy_(self.fields[src])
+
     def residual(self, idx):
         """(sum r^2, max|r|) of field buffer ``idx`` (synchronous)."""
         with self._on():

@@ -13,9 +13,9 @@ mirror / periodic / face-Dirichlet faces run one sweep per launch followed by
 a device ghost refresh), constant or per-cell coefficients, optional mask,
 optional nonlinear source, ``post_sweep`` hooks that copy field values (e.g.
 the spherical ``tie_origin``; applied on the device as a gather after every
-sweep, ``post_sweep_gather``).  Hooks that compute values, 1-D grids and the
-Gauss-Seidel/SOR solvers raise ``NotImplementedError`` -- there is no CPU
-fallback.
+sweep, ``post_sweep_gather``), and Gauss-Seidel / SOR as a bitwise GPU
+wavefront (``srj_plan_gs``).  Hooks that compute values and 1-D grids raise
+``NotImplementedError`` -- there is no CPU fallback.
 
 Entry points and the reference code they replace:
 
@@ -466,13 +466,79 @@ def jacobi_solve(problem, tol, max_iters=10_000_000, *, stop="update_inf",
 
 
 def gauss_seidel_solve(problem, tol, max_iters=10_000_000):
-    """Lexicographic Gauss-Seidel is sequential by definition (SPEC.md:301);
-    a GPU red-black variant would change the iterates, so it is out of scope."""
-    raise NotImplementedError("gauss_seidel_solve is not on the GPU path")
+    """Gauss-Seidel in lexicographic order (``grids.py:697-702``), bitwise the
+    reference's in-place ``_gs2``/``_gs3`` sweeps, on a GPU wavefront
+    (``srj_plan_gs``).  Same returns, stopping rule (``dmax < tol`` after every
+    sweep) and ``DivergenceError`` as the reference."""
+    return _gs_solve(problem, 1.0, tol, max_iters, sor=False)
 
 
 def sor_solve(problem, omega, tol, max_iters=10_000_000):
-    """See gauss_seidel_solve."""
+    """Successive over-relaxation (``grids.py:705-716``): Gauss-Seidel with
+    relaxation factor ``omega``; the stopping metric is ``dmax / omega``."""
     if not 0.0 < omega < 2.0:
         raise ValueError("SOR relaxation factor must lie in (0, 2)")
-    raise NotImplementedError("sor_solve is not on the GPU path")
+    return _gs_solve(problem, float(omega), tol, max_iters, sor=True)
+
+
+def _gs_solve(problem, omega, tol, max_iters, sor):
+    tol = float(tol)
+    if tol <= 0.0:
+        raise ValueError("tolerance must be positive")
+    if max_iters < 1:
+        raise ValueError("max_iters must be at least 1")
+    if getattr(problem, "source_kappa", None) is not None:
+        raise NotImplementedError("Gauss-Seidel has no nonlinear source")
+    dev = _device_grid(problem)
+    start = time.perf_counter()
+    diffs, resids, secs = [], [], []
+    converged = False
+    diverged_at = None
+    cur, work = 0, 1  # cur: snapshot at a chunk start; work: swept in place
+    done = 0
+    # chunks as in _solve, sized for the slower in-place wavefront sweeps
+    est = 8.0 * _step_seconds_estimate(problem)
+    cap = int(min(65536, max(16, 0.05 / est)))
+    span = int(min(cap, max(8, 0.002 / est)))
+    try:
+        while done < max_iters:
+            n = min(span, max_iters - done)
+            span = min(cap, 2 * span)
+            dev.copy_field(cur, work)
+            dev.gs(work, omega, n)
+            norms = dev.norms[:2 * n].view(n, 2).cpu().numpy()
+            t_now = time.perf_counter() - start
+            t_prev = float(secs[-1][-1]) if secs else 0.0
+            metric = norms[:, 0] / omega if sor else norms[:, 0]
+            bad = ~np.isfinite(metric) | (metric > OVERFLOW_LIMIT)
+            events = np.flatnonzero(bad | (metric < tol))
+            take = n if events.size == 0 else int(events[0]) + 1
+            if take < n:  # replay from the snapshot to the exact sweep
+                dev.copy_field(cur, work)
+                dev.gs(work, omega, take)
+            diffs.append(metric[:take])
+            resids.append(norms[:take, 1])
+            secs.append(t_prev + (t_now - t_prev) * np.arange(1, take + 1) / take)
+            done += take
+            cur, work = work, cur
+            if events.size:
+                if bad[take - 1]:
+                    diverged_at = take - 1
+                else:
+                    converged = True
+                break
+        dev.download_field(cur, problem.u)  # ghosts refreshed on the device
+    finally:
+        dev.close()
+    hist = ResidualHistory(
+        residual_inf=np.concatenate(diffs) if diffs else np.zeros(0),
+        true_residual_inf=np.concatenate(resids) if resids else np.zeros(0),
+        seconds=np.concatenate(secs) if secs else np.zeros(0),
+        tolerance=tol, converged=converged)
+    if diverged_at is not None:
+        hist.converged = False
+        dmax = float(hist.residual_inf[-1])
+        raise DivergenceError(
+            f"update norm {dmax:.3e} exceeds the overflow guard after "
+            f"{hist.iterations} steps", hist.iterations, hist)
+    return hist, problem.interior

@@ -660,3 +660,68 @@ def test_per_cell_coefficients_2d_streaming_kernel(masked):
     hist, _ = run_steps(p, w, 45, fuse=1, chunk=20)
     assert np.array_equal(p.u, want.u)
     assert np.array_equal(hist.true_residual_inf, norms[:, 1])
+
+
+GS_CASES = ["gs_var2d", "sor_var2d", "gs_var3d", "sor_var3d", "gs_const2d_solve", "sor_neumann2d"]
+
+
+@pytest.mark.parametrize("name", GS_CASES)
+def test_gauss_seidel_wavefront_vs_reference(name):
+    """gauss_seidel_solve / sor_solve on the GPU wavefront == the reference's
+    sequential in-place sweeps bit for bit (fields incl. ghosts, both norm
+    histories, iteration count of the tolerance run)."""
+    from conftest import rules_from
+
+    g = load_golden(name)
+    p = problem_from(fields_from(g), bc=rules_from(g))
+    kw = dict(tol=float(g["tol"]), max_iters=int(g["steps"]))
+    if bool(g["sor"]):
+        hist, _ = G.sor_solve(p, float(g["omega"]), **kw)
+    else:
+        hist, _ = G.gauss_seidel_solve(p, **kw)
+    assert np.array_equal(p.u, g["u_final"])
+    assert np.array_equal(hist.residual_inf, g["residual_inf"])
+    assert np.array_equal(hist.true_residual_inf, g["true_residual_inf"])
+    assert hist.converged == bool(g["converged"])
+
+
+@pytest.mark.parametrize("shape,omega,masked", [((700, 611), 1.0, True), ((257, 1030), 1.7, False),
+                                                ((40, 44, 36), 1.0, True), ((18, 7, 90), 1.4, False)])
+def test_gauss_seidel_wavefront_vs_oracle(shape, omega, masked):
+    """Larger grids than the fixtures: many 32-row strips (2D), strips that span
+    plane boundaries and planes shorter than a strip (3D)."""
+    rng = np.random.default_rng(11)
+    nd = len(shape)
+    f = {"u": rng.standard_normal(tuple(n + 2 for n in shape)), "source": rng.standard_normal(shape),
+         "center": 2.0 * nd + rng.random(shape),
+         "lower": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd)),
+         "upper": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd)),
+         "mask": (rng.random(shape) > 0.1) if masked else None}
+    steps = 25
+    q = problem_from(f)
+    _, _, norms = oracle.gs_solve(q, omega, steps, sor=omega != 1.0)
+    p = problem_from(f)
+    if omega == 1.0:
+        hist, _ = G.gauss_seidel_solve(p, 1e-300, max_iters=steps)
+    else:
+        hist, _ = G.sor_solve(p, omega, 1e-300, max_iters=steps)
+    assert np.array_equal(p.u, q.u)
+    assert np.array_equal(hist.residual_inf, norms[:, 0])
+    assert np.array_equal(hist.true_residual_inf, norms[:, 1])
+
+
+def test_gauss_seidel_wavefront_short_planes():
+    """3-D planes of 2..5 rows: previous-plane neighbours inside the same strip
+    are written a few steps before use (read late, not prefetched)."""
+    rng = np.random.default_rng(12)
+    for shape in ((30, 2, 50), (11, 3, 33), (9, 5, 64)):
+        f = {"u": rng.standard_normal(tuple(n + 2 for n in shape)), "source": rng.standard_normal(shape),
+             "center": 6.0 + rng.random(shape),
+             "lower": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(3)),
+             "upper": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(3)), "mask": None}
+        q = problem_from(f)
+        _, _, norms = oracle.gs_solve(q, 1.0, 15)
+        p = problem_from(f)
+        hist, _ = G.gauss_seidel_solve(p, 1e-300, max_iters=15)
+        assert np.array_equal(p.u, q.u), shape
+        assert np.array_equal(hist.true_residual_inf, norms[:, 1]), shape
