@@ -44,7 +44,7 @@ struct GSParams {
   double *norms;             // [nsweeps][2]: (dmax, rmax)
 };
 
-constexpr int kGSPublish = 8;  // publish progress every 8 steps
+constexpr int kGSPublish = 16;  // publish progress every 16 steps (the release is a full memory barrier)
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
   unsigned long long v;
@@ -172,6 +172,9 @@ __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams 
 
     double rmx = 0.0, dmx = 0.0;
     double yprev = 0.0;  // this lane's result of the previous step (column j-1)
+    // the row's ghost columns are constant during a sweep: keep them in
+    // registers so no load sits in the per-step dependency chain
+    const double ghost_l = __ldcg(u + off - 1), ghost_r = __ldcg(u + off + p.ncols);
     Ops ring[kPF + 1];
 #pragma unroll
     for (int q = 0; q <= kPF; ++q) {
@@ -192,11 +195,11 @@ __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams 
         const double upn = __shfl_up_sync(kFull, yprev, 1);  // lane r-1, step d-1 = (R-1, j)
         const double upv = need_up_mem ? cur.up_mem : upn;
         const double dnv = need_dn_mem ? cur.dn_mem : dn_sh;
-        const double left = (j == 0) ? __ldcg(u + off - 1) : yprev;
+        const double left = (j == 0) ? ghost_l : yprev;
         // own centre of step d+1 = column j+1 (old); the last column's right
         // neighbour is the ghost column (lane 31 reaches it at the sweep's
         // final step, whose successor is never loaded into the ring)
-        const double right = (j == p.ncols - 1) ? __ldcg(u + off + p.ncols) : nxt.uc;
+        const double right = (j == p.ncols - 1) ? ghost_r : nxt.uc;
         if (ND == 3 && pa_late) cur.pa = __ldcg(u + off - p.plane + clampj(j));
         double k7[1 + 2 * ND];
 #pragma unroll
