@@ -212,7 +212,8 @@ def run_gpu(args):
     base = config_fields(WORKLOAD)
     n0, n1 = base["source"].shape
     fuse = args.fuse
-    if ws > 1:
+    slab = ws > 1 or args.slab
+    if slab:
         from paper_1511_04292_b200.distributed import SlabGrid
 
         grid = SlabGrid.weak_rows(base, rank, ws, fuse=fuse or 4)
@@ -277,8 +278,11 @@ def run_gpu(args):
 
     e2e = None
     cpu = None
-    if rank == 0 and ws == 1:
+    if slab:
+        e2e = measure_e2e_slab(grid, grid.fields, cyc, args.e2e_steps, ws)
+    elif rank == 0:
         e2e = measure_e2e(G, base, cyc, args.e2e_steps)
+    if rank == 0 and ws == 1 and not slab:
         if not args.no_cpu:
             cpu = cpu_baseline(base, w)
     if ws > 1:
@@ -342,6 +346,47 @@ def measure_e2e(G, base, cyc, steps):
             "calls": steps, "api": "paper_1511_04292_b200.srj_solve(problem, cycle, tol, max_iters=M)"}
 
 
+def measure_e2e_slab(grid, fields, cyc, steps, ws):
+    """Multi-GPU e2e through the slab API: every rank uploads its slab (u with
+    halos, source) from pinned host memory, runs one cycle (halo exchanges,
+    norm all-reduce) and downloads its owned rows; wall time, max over ranks."""
+    import torch
+
+    d = grid.decomp
+    g = grid.backend.grid
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    u = pin(d.local_field(fields["u"]))
+    src = pin(d.local_interior(fields["source"]))
+    w = cyc.weight_sequence
+    m = cyc.m
+    out = None
+    times = []
+    for it in range(steps + 1):  # first call warms up
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g.upload_field(u, g.fields[0])
+        g.upload_source(src)
+        buf = grid.run(0, w, 0, m)
+        _ = grid.norms[:2 * m].numpy()
+        out = grid.backend.download_owned(buf)
+        torch.cuda.synchronize()
+        if it:
+            times.append(time.perf_counter() - t0)
+    dt = sum(times)
+    if ws > 1:
+        t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dt = float(t[0])
+    cells = grid.owned_cells * ws
+    return {"value": cells * m * steps / dt / 1e9, "unit": "GLUPS",
+            "h2d_bytes_per_step": int(u.nbytes + src.nbytes),
+            "d2h_bytes_per_step": int(out.nbytes + 16 * m),
+            "calls": steps, "api": "paper_1511_04292_b200.distributed.SlabGrid (upload, run, "
+                                   "download_owned) per rank, max over ranks"}
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -351,6 +396,8 @@ def main():
     ap.add_argument("--fuse", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--slab", action="store_true",
+                    help="use the multi-GPU slab path even on one GPU (testing)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -239,6 +239,7 @@ class SlabGrid:
         import torch
 
         n0 = fields["source"].shape[0]
+        self.fields = fields  # the global problem (host); the e2e bench re-uploads from it
         self.decomp = SlabDecomposition(n0, world, rank, halo=max(1, fuse))
         self.backend = DeviceSlab(fields, self.decomp)
         fuse = max(1, min(fuse, self.backend.max_fuse))

@@ -112,10 +112,12 @@ class DeviceGrid:
                 self._upload_interior(_contig(active, np.uint8), m, 1)
                 self._keep.append(m)
                 desc.act = m.data_ptr()
+            # the source (or kappa) in the padded layout; kept for re-uploads
+            self.f_dev = self._interior_array(kappa if kappa is not None else source)
             if kappa is not None:
-                desc.kappa = self._interior_array(kappa).data_ptr()
+                desc.kappa = self.f_dev.data_ptr()
             else:
-                desc.source = self._interior_array(source).data_ptr()
+                desc.source = self.f_dev.data_ptr()
             lo, hi = (0, self.shape[0]) if own is None else own
             desc.own0_begin = int(lo)
             desc.own0_end = int(hi)
@@ -188,6 +190,11 @@ class DeviceGrid:
     def upload_field(self, host, dev):
         with self._on():
             self._upload_field(host, dev)
+
+    def upload_source(self, host):
+        """Re-upload the source (or kappa) from an interior-shaped host array."""
+        with self._on():
+            self._upload_interior(_contig(host, np.float64), self.f_dev, 8)
 
     def _upload_field(self, host, dev):
         _lib.check(self.lib.srj_upload_field(
