@@ -154,7 +154,9 @@ __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams 
       const int64_t j = d - lane;
       const int64_t jc = clampj(j);
       const double *row = u + off;
-      o.uc = __ldcg(row + jc);
+      // own-strip rows are written only by this warp (this SM), so the L1
+      // path is coherent for them: one 128-B line serves 16 steps of a lane
+      o.uc = row[jc];
       if (need_up_mem) o.up_mem = __ldcg(row - p.pitch + jc);
       if (need_dn_mem) o.dn_mem = __ldcg(row + p.pitch + jc);
       if (ND == 3) {
