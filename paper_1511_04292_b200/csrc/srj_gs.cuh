@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams 
   // 3D, planes of < 32 rows: the previous-plane row of some lanes lies in this
   // strip and is written fewer than kPF steps before use -> read it late
   const bool pa_late = (ND == 3) && (R - p.n1 >= int64_t(s) * 32);
+  const bool pa_any = __any_sync(kFull, pa_late);  // warp-uniform
 
   // operands of one step, loaded kPF steps ahead into a register ring
   struct Ops {
@@ -178,13 +179,13 @@ __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams 
     // registers so no load sits in the per-step dependency chain
     const double ghost_l = __ldcg(u + off - 1), ghost_r = __ldcg(u + off + p.ncols);
     Ops ring[kPF + 1];
+    wait_for(kPF);  // requirements are monotone in the step: one wait covers 0..kPF
 #pragma unroll
-    for (int q = 0; q <= kPF; ++q) {
-      wait_for(q);
-      load(q, ring[q]);
-    }
+    for (int q = 0; q <= kPF; ++q) load(q, ring[q]);
 #pragma unroll 1
     for (int64_t d0 = 0; d0 < W; d0 += kPF + 1) {
+      // one progress wait per ring round, for the farthest step it prefetches
+      if (d0 + kPF + 1 < W) wait_for(min(d0 + 2 * kPF + 1, W - 1));
 #pragma unroll
       for (int q = 0; q <= kPF; ++q) {
         const int64_t d = d0 + q;
@@ -227,17 +228,14 @@ __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams 
           acc_absmax(dmx, dd);
         }
         yprev = y;
-        __syncwarp();  // this step's stores before any lane's later reads
+        if (ND == 3 && pa_any) __syncwarp();  // stores before late same-strip plane reads
         // publish (stores of every lane ordered before the release by the
         // warp barrier), then refill this slot with step d+kPF+1
         if ((d % kGSPublish) == kGSPublish - 1 || d == W - 1) {
           __syncwarp();
           if (lane == 0) st_release_u64(p.prog + s, base + d + 1);
         }
-        if (d + kPF + 1 < W) {
-          wait_for(d + kPF + 1);
-          load(d + kPF + 1, cur);
-        }
+        if (d + kPF + 1 < W) load(d + kPF + 1, cur);
       }
     }
     const double rm = warp_max(fabs(rmx));
