@@ -123,10 +123,14 @@ typedef struct {
     int32_t physical_lo0;        /* 1: layer below row 0 is a FIXED boundary  */
     int32_t physical_hi0;        /* 1: layer above row n0-1 is a FIXED bound. */
     srj_face_rule bc[3][2];      /* per axis (low, high) ghost rule; all-zero =
-                                    FIXED everywhere.  Any non-FIXED face runs
-                                    one sweep per launch followed by the ghost
-                                    refresh (BoundaryRule, grids.py:73-112,
-                                    refresh_ghosts :225-247); single-slab only */
+                                    FIXED everywhere.  Non-FIXED faces refresh
+                                    the ghosts after every launch (BoundaryRule,
+                                    grids.py:73-112, refresh_ghosts :225-247);
+                                    2D MIRROR / FACE_DIRICHLET faces fuse up to
+                                    4 sweeps per launch (the ghosts between
+                                    fused sweeps are formed on chip), PERIODIC
+                                    and 3D run one sweep per launch;
+                                    single-slab only */
 } srj_plan_desc;
 
 typedef struct srj_plan srj_plan;

@@ -138,6 +138,8 @@ int sm_count() {
 }
 
 // ------------------------------------------------------------ 2D dispatch
+constexpr int kMaxFuseBC = 4;  // 2D fused depth with MIRROR / FACE_DIRICHLET faces
+
 // One entry per kernel instantiation: launcher + resident blocks per SM
 // (registers and shared memory both counted, from the occupancy API), so the
 // launch can be sized to exactly one wave.
@@ -149,28 +151,28 @@ struct Kernel2D {
   int own;  // columns owned per band
 };
 
-template <int T, bool VAR, bool NL, bool RECIP>
+template <int T, bool VAR, bool NL, bool RECIP, int BCF = 0>
 struct K2 {
   static constexpr int V = 2;
   using B = Band2D<T, V>;
   static void configure() {
     static std::atomic<uint64_t> done{0};
     once_per_device(done, [] {
-      cudaFuncSetAttribute(sweep2d_tb<T, V, VAR, NL, RECIP>,
+      cudaFuncSetAttribute(sweep2d_tb<T, V, VAR, NL, RECIP, BCF>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(B::smem_bytes()));
     });
   }
   static void launch(const Sweep2DParams &p, const CUtensorMap &tu, const CUtensorMap &tf,
                      int blocks, cudaStream_t s) {
     configure();
-    sweep2d_tb<T, V, VAR, NL, RECIP><<<blocks, B::WARPS * 32, B::smem_bytes(), s>>>(p, tu, tf);
+    sweep2d_tb<T, V, VAR, NL, RECIP, BCF><<<blocks, B::WARPS * 32, B::smem_bytes(), s>>>(p, tu, tf);
   }
   static int bps() {
     static std::atomic<int> cache[kMaxDevices];
     return cached_per_device(cache, [] {
       configure();
       int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_tb<T, V, VAR, NL, RECIP>,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_tb<T, V, VAR, NL, RECIP, BCF>,
                                                     B::WARPS * 32, B::smem_bytes());
       return n > 0 ? n : 1;
     });
@@ -178,8 +180,21 @@ struct K2 {
   static Kernel2D get() { return Kernel2D{launch, B::BAND, bps, B::OWN}; }
 };
 
+template <int T, int BCF>
+Kernel2D pick2d_bc(bool var, bool nl, bool recip) {
+  if (var) return nl ? K2<T, true, true, false, BCF>::get() : K2<T, true, false, false, BCF>::get();
+  if (recip) return nl ? K2<T, false, true, true, BCF>::get() : K2<T, false, false, true, BCF>::get();
+  return nl ? K2<T, false, true, false, BCF>::get() : K2<T, false, false, false, BCF>::get();
+}
+
+// bcf: 0 = FIXED faces; 1 = fused MIRROR / FACE_DIRICHLET faces; 2 = the same
+// with MIRROR-or-FIXED column faces (no face values in the edge-band path)
 template <int T>
-Kernel2D pick2d_t(bool var, bool nl, bool recip) {
+Kernel2D pick2d_t(bool var, bool nl, bool recip, int bcf) {
+  if constexpr (T >= 2 && T <= kMaxFuseBC) {
+    if (bcf == 1) return pick2d_bc<T, 1>(var, nl, recip);
+    if (bcf == 2) return pick2d_bc<T, 2>(var, nl, recip);
+  }
   if (var) return nl ? K2<T, true, true, false>::get() : K2<T, true, false, false>::get();
   if (recip) return nl ? K2<T, false, true, true>::get() : K2<T, false, false, true>::get();
   return nl ? K2<T, false, true, false>::get() : K2<T, false, false, false>::get();
@@ -395,16 +410,16 @@ int make_tmap(CUtensorMap *m, const double *base, const srj_layout_t &l, int box
   return SRJ_OK;
 }
 
-Kernel2D pick2d(int T, bool var, bool nl, bool recip) {
+Kernel2D pick2d(int T, bool var, bool nl, bool recip, int bcf) {
   switch (T) {
-    case 1: return pick2d_t<1>(var, nl, recip);
-    case 2: return pick2d_t<2>(var, nl, recip);
-    case 3: return pick2d_t<3>(var, nl, recip);
-    case 4: return pick2d_t<4>(var, nl, recip);
-    case 5: return pick2d_t<5>(var, nl, recip);
-    case 6: return pick2d_t<6>(var, nl, recip);
-    case 7: return pick2d_t<7>(var, nl, recip);
-    default: return pick2d_t<8>(var, nl, recip);
+    case 1: return pick2d_t<1>(var, nl, recip, bcf);
+    case 2: return pick2d_t<2>(var, nl, recip, bcf);
+    case 3: return pick2d_t<3>(var, nl, recip, bcf);
+    case 4: return pick2d_t<4>(var, nl, recip, bcf);
+    case 5: return pick2d_t<5>(var, nl, recip, bcf);
+    case 6: return pick2d_t<6>(var, nl, recip, bcf);
+    case 7: return pick2d_t<7>(var, nl, recip, bcf);
+    default: return pick2d_t<8>(var, nl, recip, bcf);
   }
 }
 
@@ -426,9 +441,11 @@ __global__ void selftest_div(const double *a, int64_t n, double c, double y, dou
 
 struct srj_plan {
   srj_plan_desc d;
-  bool has_bc;       // some face is not FIXED: refresh ghosts after each sweep
+  bool has_bc;       // some face is not FIXED: refresh ghosts after each launch
+  bool bc_fusable;   // ...and all of them are MIRROR/FACE_DIRICHLET on a 2D grid
   int default_fuse;
   double *partials;  // [kResidBlocks][2] device scratch
+  double *bc_scalars;  // [2][2] device copies of the 2D faces' scalar values (fused BCs)
   // small-grid cluster path: per-chunk omegas (device + pinned staging)
   double *d_omegas = nullptr, *h_omegas = nullptr;
   int64_t omega_cap = 0;
@@ -575,13 +592,33 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
     delete p;
     return fail(SRJ_EUNSUPPORTED, "non-FIXED boundary rules need the whole grid on one plan");
   }
-  // non-FIXED ghosts change every step: one sweep per launch + refresh
-  p->default_fuse = (desc->coef_mode == 0 && !p->has_bc) ? (l.ndim == 2 ? 4 : 2) : 1;
+  // non-FIXED ghosts change every step.  MIRROR and FACE_DIRICHLET ghosts are a
+  // function of the adjacent cell, so the 2D band kernel folds them into its
+  // fused stages; PERIODIC (the opposite face) and 3D run one sweep per launch
+  p->bc_fusable = p->has_bc && l.ndim == 2;
+  for (int a = 0; a < l.ndim; ++a)
+    if (desc->bc[a][0].kind == SRJ_BC_PERIODIC) p->bc_fusable = false;
+  p->default_fuse = (desc->coef_mode == 0 && (!p->has_bc || p->bc_fusable))
+                        ? (l.ndim == 2 ? 4 : 2)
+                        : 1;
   p->partials = nullptr;
+  p->bc_scalars = nullptr;
   cudaError_t e = cudaMalloc(&p->partials, sizeof(double) * 2 * kResidBlocks);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "cudaMalloc(partials)");
+  }
+  if (p->bc_fusable) {
+    double v[4];
+    for (int f = 0; f < 4; ++f) v[f] = desc->bc[f >> 1][f & 1].value;
+    e = cudaMalloc(&p->bc_scalars, sizeof(v));
+    if (e == cudaSuccess) e = cudaMemcpy(p->bc_scalars, v, sizeof(v), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(p->partials);
+      if (p->bc_scalars) cudaFree(p->bc_scalars);
+      delete p;
+      return cuda_fail(e, "cudaMalloc(bc scalars)");
+    }
   }
   *out = p;
   return SRJ_OK;
@@ -624,6 +661,7 @@ int srj_plan_destroy(srj_plan *p) {
   free_gather(p);
   if (p->gs_prog) cudaFree(p->gs_prog);
   if (p->partials) cudaFree(p->partials);
+  if (p->bc_scalars) cudaFree(p->bc_scalars);
   if (p->d_omegas) cudaFree(p->d_omegas);
   if (p->h_omegas) cudaFreeHost(p->h_omegas);
   if (p->omega_ev) cudaEventDestroy(p->omega_ev);
@@ -824,7 +862,9 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
   const srj_layout_t &l = d.layout;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int T = fuse > 0 ? fuse : plan->default_fuse;
-  if (plan->has_bc || plan->g_n > 0 || (l.ndim == 3 && d.coef_mode == 1)) T = 1;
+  if ((plan->has_bc && !plan->bc_fusable) || plan->g_n > 0 || (l.ndim == 3 && d.coef_mode == 1))
+    T = 1;
+  if (plan->has_bc && T > kMaxFuseBC) T = kMaxFuseBC;
   if (l.ndim == 3 && T > kMaxFuse3D) T = kMaxFuse3D;
   if (T > kMaxFuse) return fail(SRJ_EINVAL, "fuse depth %d exceeds %d", T, kMaxFuse);
   if ((!d.physical_lo0 || !d.physical_hi0) && T > l.halo0)
@@ -882,7 +922,13 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.ld_hi = ld_hi;
       p.own_b = int(d.own0_begin);
       p.own_e = int(d.own0_end);
-      const Kernel2D k2 = pick2d(t, var, nl, !var && p.kinv != 0.0);
+      int bcf = 0;
+      if (plan->has_bc && t > 1) {
+        bcf = 2;
+        for (int side = 0; side < 2; ++side)
+          if (d.bc[1][side].kind == SRJ_BC_FACE_DIRICHLET) bcf = 1;
+      }
+      const Kernel2D k2 = pick2d(t, var, nl, !var && p.kinv != 0.0, bcf);
       p.nbands = int((l.n[1] + k2.own - 1) / k2.own);
       // strips x bands = waves x resident warps (default one wave)
       const int bps = bps_override() > 0 ? std::min(bps_override(), k2.blocks_per_sm())
@@ -896,6 +942,14 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.norms = d_norms + 2 * k;
       p.tma_col0 = int(l.origin + 1);
       p.tma_row0 = l.halo0;
+      for (int a = 0; a < 2; ++a)
+        for (int side = 0; side < 2; ++side) {
+          const srj_face_rule &b = d.bc[a][side];
+          p.bc_kind[a][side] = b.kind;
+          const bool arr = b.kind == SRJ_BC_FACE_DIRICHLET && b.values;
+          p.bc_ptr[a][side] = arr ? b.values : plan->bc_scalars + 2 * a + side;
+          p.bc_step[a][side] = arr ? 1 : 0;
+        }
       CUtensorMap tu, tf;
       int rc = make_tmap(&tu, cur, l, k2.box_cols);
       if (rc != SRJ_OK) return rc;

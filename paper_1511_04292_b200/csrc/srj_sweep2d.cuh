@@ -58,6 +58,12 @@ struct Sweep2DParams {
   int tma_row0;        // tensor-map row of interior row 0
   double omega[kMaxFuse];
   double *norms;       // [T][2]: (dmax, rmax) per fused step
+  // MIRROR / FACE_DIRICHLET faces under fusion (kernel flag BCF): between
+  // stages the window's ghost cells are set to the ghost the reference
+  // refreshes after every sweep, a pure function of the adjacent cell
+  int bc_kind[2][2];           // SRJ_BC_* per (axis, side)
+  const double *bc_ptr[2][2];  // face_dirichlet value at face position q: bc_ptr[q * bc_step]
+  int bc_step[2][2];           // 1: per-position array; 0: the face's scalar
 };
 
 template <int T, int V_ = 2>
@@ -82,12 +88,12 @@ struct Band2D {
 // hold stage t-1 rows r-1, r, r+1, all produced in earlier ticks, so the T
 // stages of a tick are mutually independent.  Writes the stage-t value of row
 // r to y and the numerators to num; bad collects div_recip range failures.
-template <bool FAST, bool EDGE, bool VAR, bool NL, bool RECIP, int V>
+template <bool FAST, bool EDGE, bool VAR, bool NL, bool RECIP, int SUB, int V>
 __device__ __forceinline__ void stage2d(const Sweep2DParams &p, const double (&up)[V],
                                         const double (&mid)[V], const double (&down)[V],
                                         const double *frow, int r, double om, int lane_col,
                                         int i0, int i1, int own_c0, int own_c1, int f_lo,
-                                        int f_hi, unsigned colact, bool cnt, double (&y)[V],
+                                        int f_hi, unsigned colact, bool cnt, unsigned bcm, double (&y)[V],
                                         double (&num)[V], double &rmx, double &dmx, bool &bad) {
   double fv[V];
 #pragma unroll
@@ -98,6 +104,29 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, const double (&u
   }
   const double west0 = __shfl_up_sync(kFull, mid[V - 1], 1);
   const double eastV = __shfl_down_sync(kFull, mid[0], 1);
+  // SUB (fused MIRROR / FACE_DIRICHLET column faces; bcm = 0 for stage 1,
+  // which reads the refreshed ghosts from memory): column 0's
+  // west and column n1-1's east neighbours are the ghosts the per-sweep
+  // refresh would hold, computed here from the cell itself.  Branch-free and
+  // off the critical path: resid5 consumes them last.
+  double gw = 0.0, ge = 0.0;
+  if (SUB) {
+    static_assert(V == 2, "east-face cell select assumes two cells per lane");
+    if (r < 0 || r >= p.n0) bcm = 0;  // ghost rows (slow ticks): corners untouched
+    const double ae = (bcm & 4u) ? mid[1] : mid[0];
+    if (SUB == 2) {  // column faces MIRROR (or FIXED): the cell itself
+      gw = mid[0];
+      ge = ae;
+    } else {
+      const int rq = min(max(r, 0), p.n0 - 1);
+      const double vw = __ldg(p.bc_ptr[1][0] + int64_t(rq) * p.bc_step[1][0]);
+      const double ve = __ldg(p.bc_ptr[1][1] + int64_t(rq) * p.bc_step[1][1]);
+      const double fw = __dsub_rn(__dmul_rn(2.0, vw), mid[0]);
+      const double fe = __dsub_rn(__dmul_rn(2.0, ve), ae);
+      gw = p.bc_kind[1][0] == 1 ? mid[0] : fw;
+      ge = p.bc_kind[1][1] == 1 ? ae : fe;
+    }
+  }
   bool row_act = true, row_own = true;
   int rc = 0;
   if (!FAST) {
@@ -110,8 +139,12 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, const double (&u
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const double uc = mid[v];
-    const double uw = (v == 0) ? west0 : mid[v - 1];
-    const double ue = (v == V - 1) ? eastV : mid[v + 1];
+    double uw = (v == 0) ? west0 : mid[v - 1];
+    double ue = (v == V - 1) ? eastV : mid[v + 1];
+    if (SUB) {
+      if (v == 0 && (bcm & 1u)) uw = gw;
+      if ((bcm >> (1 + v)) & 1u) ue = ge;
+    }
     double c = p.kc, a0 = p.kam0, b0 = p.kap0, a1 = p.kam1, b1 = p.kap1;
     bool act = true;
     const int col = lane_col + v;
@@ -179,6 +212,15 @@ __device__ __forceinline__ void fix_stage(const Sweep2DParams &p, const double (
   }
 }
 
+// The refreshed ghost next to boundary cell value adj at face position q
+// (ghost_refresh's arithmetic, srj_reduce.cuh).
+__device__ __forceinline__ double bc_ghost(const Sweep2DParams &p, int ax, int side, double adj,
+                                           int q) {
+  if (p.bc_kind[ax][side] == 1) return adj;
+  const double v = __ldg(p.bc_ptr[ax][side] + int64_t(q) * p.bc_step[ax][side]);
+  return __dsub_rn(__dmul_rn(2.0, v), adj);
+}
+
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
                                             uint64_t *bar) {
   asm volatile(
@@ -192,7 +234,7 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-template <int T, int V, bool VAR, bool NL, bool RECIP>
+template <int T, int V, bool VAR, bool NL, bool RECIP, int BCF>
 __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
     sweep2d_tb(const __grid_constant__ Sweep2DParams p, const __grid_constant__ CUtensorMap tm_u,
                const __grid_constant__ CUtensorMap tm_f) {
@@ -253,6 +295,16 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
     if (lane_col + v >= 0 && lane_col + v < p.n1) colact |= 1u << v;
     if (lane_col + v >= own_c0 && lane_col + v < own_c1) colact |= 1u << (V + v);
   }
+  // fused non-FIXED column faces at this lane's cells: bit 0 = column 0 (at
+  // v = 0, since TP is a multiple of V), bit 1+v = column n1-1 at v
+  unsigned bcm = 0;
+  if (BCF) {
+    if (lane_col == 0 && p.bc_kind[1][0]) bcm |= 1u;
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (lane_col + v == p.n1 - 1 && p.bc_kind[1][1]) bcm |= 2u << v;
+  }
+  const bool warp_sub = BCF && __any_sync(kFull, bcm != 0);
   const int tma_col = p.tma_col0 + col_band;
   const int tma_row = p.tma_row0 + rho_b;
 
@@ -302,16 +354,37 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
       const bool fast_rows = rho >= fast_lo && rho <= fast_hi;
       // stages in descending order: stage t reads its window, then stage t-1
       // writes its output into stage t's free window row (no register copies)
-#define SRJ_STAGE(FASTV, EDGEV)                                                                      \
+// BCF row-face fix-up after the stages of a slow tick: stage t's output row
+// r = rho-2t (w[t+1][ph%3]; row r-1 in w[t+1][(ph+2)%3]) feeds stage t+1, so
+// the ghost rows -1 / n0 in that window get the values the per-sweep refresh
+// would give them (stage T's row is stored; the ghost kernel refreshes memory
+// after the launch).  Rows 0 and n0-1 meet stages >= 2 in slow ticks only.
+#define SRJ_BCFIX                                                                             \
+  _Pragma("unroll") for (int t = 1; t < T; ++t) {                                             \
+    const int r = rho - 2 * t;                                                                \
+    double(&cur)[V] = w[t + 1][ph % 3];                                                       \
+    double(&prv)[V] = w[t + 1][(ph + 2) % 3];                                                 \
+    if (r == 0 && p.bc_kind[0][0]) { /* row -1, already in the window */                      \
+      _Pragma("unroll") for (int v = 0; v < V; ++v) if ((colact >> v) & 1u) prv[v] =          \
+          bc_ghost(p, 0, 0, cur[v], lane_col + v);                                            \
+    }                                                                                         \
+    if (r == p.n0 && p.bc_kind[0][1]) { /* row n0, just passed through */                     \
+      _Pragma("unroll") for (int v = 0; v < V; ++v) if ((colact >> v) & 1u) cur[v] =          \
+          bc_ghost(p, 0, 1, prv[v], lane_col + v);                                            \
+    }                                                                                         \
+  }
+#define SRJ_STAGE(FASTV, EDGEV, SUBV)                                                                 \
   _Pragma("unroll") for (int t = T; t >= 1; --t) {                                            \
     const int fg = g + ((ph - 2 * t) >= 0 ? 0 : -((2 * t - ph + G - 1) / G));                 \
     const int fr = ph - 2 * t + G * (g - fg);                                                 \
     const double *frow = ring_f + (fg & (NF - 1)) * BOXD + fr * BAND + V * lane;              \
     double(&dst)[V] = (t == T) ? yT : w[t + 1][ph % 3];                                       \
-    stage2d<FASTV, EDGEV, VAR, NL, RECIP, V>(p, w[t][ph % 3], w[t][(ph + 1) % 3],            \
+    stage2d<FASTV, EDGEV, VAR, NL, RECIP, SUBV, V>(p, w[t][ph % 3],                          \
+                                      w[t][(ph + 1) % 3],                                     \
                                       w[t][(ph + 2) % 3], frow, rho - 2 * t, p.omega[t - 1],  \
                                       lane_col, i0, i1, own_c0, own_c1, f_lo, f_hi, colact,   \
-                                      rho - 2 * t >= i0 && rho - 2 * t < i1, dst, num[t],     \
+                                      rho - 2 * t >= i0 && rho - 2 * t < i1, t >= 2 ? bcm : 0u,  \
+                                      dst, num[t],                                            \
                                       rmx[t - 1], dmx[t - 1], bad);                           \
   }                                                                                           \
   if (RECIP && __any_sync(kFull, bad)) {                                                      \
@@ -322,12 +395,18 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
     }                                                                                         \
   }
       if (band_interior && fast_rows) {
-        SRJ_STAGE(true, false)
+        SRJ_STAGE(true, false, 0)
       } else if (band_edge && fast_rows) {
-        SRJ_STAGE(true, true)
+        if (BCF && warp_sub) {
+          SRJ_STAGE(true, true, BCF)
+        } else {
+          SRJ_STAGE(true, true, 0)
+        }
       } else {
-        SRJ_STAGE(false, false)
+        SRJ_STAGE(false, false, BCF)
+        if (BCF) SRJ_BCFIX
       }
+#undef SRJ_BCFIX
 #undef SRJ_STAGE
       {  // stage 0: the freshly loaded row enters stage 1's window
         const double *urow = ring_u + (g & (NU - 1)) * BOXD + ph * BAND + V * lane;

@@ -1,0 +1,109 @@
+"""Fused multi-sweep launches with MIRROR / FACE_DIRICHLET faces (2D).
+
+The band kernel relaxes stages 2..T of a launch against the ghost the
+reference refreshes after every sweep (grids.py:225-247), computed from the
+boundary-adjacent cell inside the stage; the ghost layer itself is refreshed
+once per launch.  Each case is compared bit for bit with the oracle's
+step-by-step sweep + refresh (``oracle.run_bc``).  Grids are above the
+small-grid cluster threshold (2^18 cells) so the band kernel runs; the shapes
+put the boundary columns at every lane/cell position of the edge bands and
+include grids of one band and of few rows.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import Cycle, problem_from
+from paper_1511_04292_b200 import grids as G
+
+pytestmark = pytest.mark.gpu
+
+W = np.array([7.3, 0.61, 0.93, 0.55, 0.97, 0.72, 0.88, 0.51, 0.99])
+
+
+def _fields(shape, seed, var=False, masked=False):
+    rng = np.random.default_rng(seed)
+    f = {"u": rng.standard_normal(tuple(n + 2 for n in shape)),
+         "source": rng.standard_normal(shape), "mask": None}
+    if var:
+        f["center"] = 4.0 + rng.random(shape)
+        f["lower"] = tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(2))
+        f["upper"] = tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(2))
+        if masked:
+            f["mask"] = rng.random(shape) > 0.1
+    else:
+        f["center"] = np.full(shape, 4.0)
+        f["lower"] = tuple(np.full(shape, -1.0) for _ in range(2))
+        f["upper"] = tuple(np.full(shape, -1.0) for _ in range(2))
+    return f
+
+
+def _rule(kind, val):
+    return G.face_dirichlet(val) if kind == "face_dirichlet" else G.BoundaryRule(kind)
+
+
+def _run(shape, bc, fuse, steps, seed, var=False, masked=False):
+    f = _fields(shape, seed, var, masked)
+    rules = tuple(tuple(_rule(k, v) for k, v in pair) for pair in bc)
+    p = problem_from(f, bc=rules)
+    q = problem_from(f)
+    q.u[...] = p.u  # same refreshed starting ghosts
+    hist, _ = G.srj_solve(p, Cycle(W), 1e-300, max_iters=steps, fuse=fuse, chunk=11)
+    _, _, norms = oracle.run_bc(q, bc, W, steps)
+    assert np.array_equal(p.u, q.u), (shape, bc, fuse)
+    metric = norms[:, 0] / np.abs(W[np.arange(steps) % len(W)])
+    assert np.array_equal(hist.residual_inf, metric)
+    assert np.array_equal(hist.true_residual_inf, norms[:, 1])
+
+
+M, F = "mirror", "face_dirichlet"
+X = "fixed"
+
+
+def _vals(n, seed):
+    return np.random.default_rng(seed).standard_normal(n)
+
+
+CASES = [
+    # (shape, bc) -- bc per axis: ((lo kind, lo value), (hi kind, hi value))
+    ((600, 517), (((M, None), (M, None)), ((M, None), (M, None)))),
+    ((533, 601), (((F, 0.75), (F, -1.25)), ((F, 2.0), (F, 0.5)))),
+    ((541, 509), (((F, _vals(509, 1)), (M, None)), ((X, None), (F, _vals(541, 2))))),
+    ((517, 531), (((X, None), (F, _vals(531, 3))), ((M, None), (X, None)))),
+    ((4100, 70), (((M, None), (F, -0.5)), ((F, _vals(4100, 4)), (M, None)))),  # few bands
+    ((2900, 100), (((M, None), (M, None)), ((M, None), (F, 1.5)))),
+    ((9, 30001), (((M, None), (F, _vals(30001, 5))), ((M, None), (M, None)))),  # few rows
+    ((40, 7001), (((F, 0.25), (M, None)), ((F, -3.0), (F, 3.0)))),
+]
+
+
+@pytest.mark.parametrize("fuse", [2, 3, 4])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_fused_mirror_face_dirichlet_constant(case, fuse):
+    shape, bc = CASES[case]
+    _run(shape, bc, fuse, 13, seed=10 * case + fuse)
+
+
+@pytest.mark.parametrize("masked", [False, True])
+@pytest.mark.parametrize("case", [0, 2, 4])
+def test_fused_mirror_face_dirichlet_per_cell(case, masked):
+    shape, bc = CASES[case]
+    _run(shape, bc, 3, 10, seed=100 + case, var=True, masked=masked)
+
+
+def test_default_fuse_neumann_laplace_matches_one_sweep_per_launch():
+    """Size-independent property at a production size: the automatic fused
+    depth and fuse=1 (one sweep + refresh per launch) agree bit for bit."""
+    from paper_1511_04292_b200.problems import laplace_neumann_fields
+
+    f = laplace_neumann_fields(2048)
+    rng = np.random.default_rng(7)
+    f["u"] = rng.standard_normal(f["u"].shape)
+    out = []
+    for fuse in (0, 1):
+        p = problem_from(dict(f), bc=((G.MIRROR, G.MIRROR),) * 2)
+        hist, _ = G.srj_solve(p, Cycle(W), 1e-300, max_iters=45, fuse=fuse)
+        out.append((p.u.copy(), hist.residual_inf.copy(), hist.true_residual_inf.copy()))
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)

@@ -25,13 +25,13 @@ from paper_1511_04292_b200.tables import shipped_table  # noqa: E402
 PEAK = 6555.5
 
 
-def measure(f, w, steps, fuse, warm=2):
+def measure(f, w, steps, fuse, warm=2, bc=None):
     """GLUPS of ``steps`` sweeps of the cycle from the initial field.  Every run
     starts from buffer 0, which srj_plan_run never writes (chunk snapshot), so
     warm-up and timed runs see the same input (a run started from another
     buffer ping-pongs through buffer 0)."""
     dev = DeviceGrid(f["u"], f["source"], f["center"], f["lower"], f["upper"],
-                     kappa=f.get("kappa"))
+                     kappa=f.get("kappa"), bc=bc)
     cells = int(np.prod(f["source"].shape))
     for _ in range(warm):
         dev.run(0, w, 0, min(steps, 64), fuse)
@@ -55,14 +55,21 @@ def main():
     ap.add_argument("--steps", type=int, default=480)
     ap.add_argument("--three", default="512,256")
     ap.add_argument("--nl", type=int, default=1)
+    ap.add_argument("--bc", default="", help="2D faces: mirror | face_dirichlet (all four)")
     a = ap.parse_args()
+    bc = None
+    if a.bc:
+        from paper_1511_04292_b200 import grids as G
+
+        rule = G.MIRROR if a.bc == "mirror" else G.face_dirichlet(0.5)
+        bc = ((rule, rule),) * 2
     tab = shipped_table()
     w = quantize(tab.lookup(6, 4096)).weight_sequence
     f = config_fields("cfg2", (a.n, a.n))
     out = []
     for fuse in [int(x) for x in a.fuse.split(",") if x]:
-        ms, g, frac = measure(f, w, a.steps, fuse)
-        r = dict(kind="2d", n=a.n, fuse=fuse, ms_per_sweep=ms, glups=g, frac_alg=frac)
+        ms, g, frac = measure(f, w, a.steps, fuse, bc=bc)
+        r = dict(kind="2d" + ("-" + a.bc if a.bc else ""), n=a.n, fuse=fuse, ms_per_sweep=ms, glups=g, frac_alg=frac)
         print(json.dumps(r), flush=True)
         out.append(r)
     for n in [int(x) for x in a.three.split(",") if x]:
