@@ -129,10 +129,14 @@ __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams 
     // wait until step d's operands are final (lane 0 polls, warp-uniform)
     auto wait_for = [&](int64_t d) {
       if (lane == 0) {
-        if (s > 0 && d < p.ncols)  // (a) previous strip's last row, this sweep
-          have_up = wait_ge(p.prog + s - 1, base + d + 32, have_up);
-        if (k > 0 && s + 1 < p.nstrips && d - 31 >= 0 && d - 31 < p.ncols)  // (b) next strip
-          have_dn = wait_ge(p.prog + s + 1, base - W + (d - 31) + 1, have_dn);
+        // (the column is clamped to the last one, not skipped: one call
+        // covers every step up to d, so the requirement must be monotone)
+        const int64_t jl = min(d, int64_t(p.ncols) - 1);
+        if (s > 0)  // (a) previous strip's last row, this sweep
+          have_up = wait_ge(p.prog + s - 1, base + jl + 32, have_up);
+        if (k > 0 && s + 1 < p.nstrips && d - 31 >= 0)  // (b) next strip
+          have_dn = wait_ge(p.prog + s + 1, base - W + min(d - 31, int64_t(p.ncols) - 1) + 1,
+                            have_dn);
         if (ND == 3) {
           // (c) previous plane, this sweep: rows R-n1 finished column d-lane
           // by their step <= d+31 (capped at the end of the sweep -- never

@@ -107,3 +107,27 @@ def test_default_fuse_neumann_laplace_matches_one_sweep_per_launch():
         out.append((p.u.copy(), hist.residual_inf.copy(), hist.true_residual_inf.copy()))
     for a, b in zip(*out):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_fused_faces(seed):
+    """Random shapes (band-kernel sizes), face kinds, scalar or per-position
+    face values, fused depth 2..4 and coefficient mode."""
+    rng = np.random.default_rng(500 + seed)
+    n0 = int(rng.integers(8, 1200))
+    n1 = int(rng.integers(max(8, (1 << 18) // n0 + 1), (1 << 18) // n0 + 900))
+    bc = []
+    for ax, n_other in ((0, n1), (1, n0)):
+        pair = []
+        for _ in range(2):
+            k = ("fixed", "mirror", "face_dirichlet")[int(rng.integers(0, 3))]
+            v = None
+            if k == "face_dirichlet":
+                v = rng.standard_normal(n_other) if rng.random() < 0.5 else float(rng.standard_normal())
+            pair.append((k, v))
+        bc.append(tuple(pair))
+    if all(k == "fixed" for pair in bc for k, _ in pair):
+        bc[1] = (("mirror", None), bc[1][1])
+    var = bool(rng.random() < 0.3)
+    _run((n0, n1), tuple(bc), int(rng.integers(2, 5)), int(rng.integers(3, 20)), seed=900 + seed,
+         var=var, masked=var and bool(rng.random() < 0.5))

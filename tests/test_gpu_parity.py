@@ -725,3 +725,29 @@ def test_gauss_seidel_wavefront_short_planes():
         hist, _ = G.gauss_seidel_solve(p, 1e-300, max_iters=15)
         assert np.array_equal(p.u, q.u), shape
         assert np.array_equal(hist.true_residual_inf, norms[:, 1]), shape
+
+
+@pytest.mark.parametrize("nd", [2, 3])
+def test_gauss_seidel_wavefront_narrow_rows(nd):
+    """Rows of 1..9 columns: each progress wait covers up to kPF+1 prefetched
+    steps, so its requirement must stay monotone past the last column (a wait
+    skipped there let lane 0 read the previous strip's row early -- random
+    seeds 278 and 315 of test_gpu_random at SRJ_RANDOM_CASES=400).  Many short
+    strips keep neighbouring strips close in time, where a missing wait shows."""
+    rng = np.random.default_rng(13 + nd)
+    for ncols in range(1, 10 if nd == 2 else 7):
+        shape = (3000, ncols) if nd == 2 else (40, 60, ncols)
+        f = {"u": rng.standard_normal(tuple(n + 2 for n in shape)),
+             "source": rng.standard_normal(shape), "center": 2.0 * nd + rng.random(shape),
+             "lower": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd)),
+             "upper": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd)), "mask": None}
+        for omega in (1.0, 1.3):
+            q = problem_from(f)
+            _, _, norms = oracle.gs_solve(q, omega, 12, sor=omega != 1.0)
+            p = problem_from(f)
+            if omega == 1.0:
+                hist, _ = G.gauss_seidel_solve(p, 1e-300, max_iters=12)
+            else:
+                hist, _ = G.sor_solve(p, omega, 1e-300, max_iters=12)
+            assert np.array_equal(p.u, q.u), (shape, omega)
+            assert np.array_equal(hist.true_residual_inf, norms[:, 1]), (shape, omega)
