@@ -82,6 +82,24 @@ class SlabDecomposition:
         a, b = self.local_rows
         return a_global[a:b]
 
+    def row_parts(self):
+        """(edges, inner): owned local interior row ranges [a, b).  ``edges``
+        are the rows the neighbours need (sent after every launch), ``inner``
+        the rest (None when the slab is all edge).  The overlapped solver
+        relaxes the edges first, starts the exchange, then relaxes the inner
+        rows while the halo rows travel."""
+        lo, hi = self.own_local
+        a = lo + (self.halo if self.rank > 0 else 0)
+        b = hi - (self.halo if self.rank < self.world - 1 else 0)
+        if a >= b:
+            return [(lo, hi)], None
+        edges = []
+        if a > lo:
+            edges.append((lo, a))
+        if b < hi:
+            edges.append((b, hi))
+        return edges, (a, b)
+
     # Exchange plan in LOCAL LAYER indices of the ghosted local field
     # (layer = local interior row + 1).
     def sends(self):
@@ -109,27 +127,41 @@ class SlabSolver:
     """Drives a slab backend: fused launches, halo exchange, norm all-reduce.
 
     backend methods:
-      reserve(nsteps) -- size the per-step norm buffer for a chunk
-      run(src, dst, weights, first, nsteps, norms_offset) -- nsteps <= fuse
-          sweeps from buffer src into buffer dst, per-step norms of OWNED rows
-          written at norms_offset of its norm buffer
+      reserve(nsteps) -- size the per-step norm buffers for a chunk
+      run(src, dst, weights, first, nsteps, norms_offset, rows=None) -- nsteps
+          <= fuse sweeps from buffer src into buffer dst; rows=None relaxes and
+          stores every owned row, rows=(a, b) only local rows [a, b) (the
+          edge / inner split); per-step norms of those rows are folded (MAX)
+          into the chunk's norm buffer at norms_offset
       layers(buf, first_layer, count) -> contiguous tensor view of layers
       norms(nsteps) -> tensor [nsteps, 2] (dmax, rmax) of the last chunk
+      comm() -> context manager for the exchange (a side CUDA stream on GPU)
+      comm_fence() -> order the main stream after the exchange (GPU)
+
+    ``overlap`` (default on when the world has neighbours; SRJ_SLAB_OVERLAP=0
+    turns it off): every launch is split into the edge rows the neighbours
+    need and the inner rows; the halo exchange runs on the comm stream
+    concurrently with the inner launch.  Edge and inner rows are
+    disjoint and the exchange touches only edge rows (sent) and halo rows
+    (received) of the destination buffer, so the split changes no value.
     """
 
-    def __init__(self, backend, decomp, group=None, fuse=4):
+    def __init__(self, backend, decomp, group=None, fuse=4, overlap=None):
+        import os
+
         if fuse > max(1, decomp.halo) and decomp.world > 1:
             raise ValueError(f"fuse depth {fuse} exceeds halo {decomp.halo}")
         self.b = backend
         self.d = decomp
         self.group = group
         self.fuse = int(fuse)
+        if overlap is None:
+            overlap = os.environ.get("SRJ_SLAB_OVERLAP", "1") != "0"
+        self.overlap = bool(overlap) and decomp.world > 1
 
-    def exchange(self, buf):
+    def _post_exchange(self, buf):
         import torch.distributed as dist
 
-        if self.d.world == 1:
-            return
         ops = []
         for peer, first, count in self.d.recvs():
             ops.append(dist.P2POp(dist.irecv, self.b.layers(buf, first, count), peer,
@@ -137,7 +169,12 @@ class SlabSolver:
         for peer, first, count in self.d.sends():
             ops.append(dist.P2POp(dist.isend, self.b.layers(buf, first, count), peer,
                                   group=self.group))
-        for req in dist.batch_isend_irecv(ops):
+        return dist.batch_isend_irecv(ops)
+
+    def exchange(self, buf):
+        if self.d.world == 1:
+            return
+        for req in self._post_exchange(buf):
             req.wait()
 
     def run(self, src, weights, first, nsteps):
@@ -153,11 +190,24 @@ class SlabSolver:
         self.b.reserve(nsteps)
         others = [i for i in range(3) if i != src]
         cur, k, flip = src, 0, 0
+        edges, inner = self.d.row_parts() if self.overlap else (None, None)
         while k < nsteps:
             t = min(self.fuse, nsteps - k)
             dst = others[flip]
-            self.b.run(cur, dst, weights, first + k, t, k)
-            self.exchange(dst)
+            if not self.overlap:
+                self.b.run(cur, dst, weights, first + k, t, k)
+                self.exchange(dst)
+            else:
+                for rows in edges:
+                    self.b.run(cur, dst, weights, first + k, t, k, rows=rows)
+                with self.b.comm():
+                    reqs = self._post_exchange(dst)
+                if inner is not None:
+                    self.b.run(cur, dst, weights, first + k, t, k, rows=inner)
+                with self.b.comm():
+                    for req in reqs:
+                        req.wait()
+                self.b.comm_fence()
             cur, flip, k = dst, 1 - flip, k + t
         norms = self.b.norms(nsteps)
         if self.d.world > 1:
@@ -186,28 +236,54 @@ class DeviceSlab:
         self.stream = self.grid.stream
         # deepest single-launch fusion the plan runs (libsrj srj_plan_run)
         self.max_fuse = (4 if self.grid.ndim == 2 else 3) if self.grid.constant else 1
+        self._part_norms = None
+        self._comm = None
+        edges, _ = decomp.row_parts()
+        self._first_part = edges[0]  # the overlapped solver runs the edges first
 
     def reserve(self, nsteps):
+        torch = self.grid.torch
         self.grid.ensure_norms(nsteps)
+        if self._part_norms is None or self._part_norms.numel() < 2 * nsteps:
+            self._part_norms = torch.zeros(2 * max(nsteps, 1), dtype=torch.float64,
+                                           device=self.grid.device)
 
-    def run(self, src, dst, weights, first, nsteps, norms_offset):
-        import ctypes
+    def run(self, src, dst, weights, first, nsteps, norms_offset, rows=None):
+        g = self.grid
+        if rows is None:
+            g.run_single(g.plan, src, dst, weights, first, nsteps,
+                         g.norms[2 * norms_offset:])
+            return
+        # edge / inner launch: its own plan over the same fields; per-step
+        # norms folded into the chunk buffer (the first part of a launch
+        # overwrites, later ones take the MAX -- exact, order-free)
+        part = self._part_norms[:2 * nsteps]
+        g.run_single(g.sub_plan(*rows), src, dst, weights, first, nsteps, part)
+        with g._on(), g.torch.cuda.stream(g.stream):
+            view = g.norms[2 * norms_offset:2 * (norms_offset + nsteps)]
+            if rows == self._first_part:
+                view.copy_(part)
+            else:
+                g.torch.maximum(view, part, out=view)
 
-        from . import _lib
+    def comm(self):
+        """Exchange context: the comm stream, ordered after the work queued
+        so far on the main stream (the edge launches)."""
+        import contextlib
 
         g = self.grid
-        spare = [i for i in range(3) if i not in (src, dst)][0]
-        w = np.ascontiguousarray(weights, dtype=np.float64)
-        out = ctypes.c_int32(0)
-        f = g.fields
-        _lib.check(g.lib.srj_plan_run(
-            g.plan, ctypes.c_void_p(f[src].data_ptr()), ctypes.c_void_p(f[dst].data_ptr()),
-            ctypes.c_void_p(f[spare].data_ptr()),
-            w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(w), int(first), int(nsteps),
-            int(nsteps), ctypes.c_void_p(g.norms.data_ptr() + 16 * norms_offset),
-            ctypes.byref(out), g._sp), "srj_plan_run")
-        if out.value != 1:
-            raise RuntimeError("slab launch must be a single fused launch (fuse >= nsteps)")
+        torch = g.torch
+        if self._comm is None:
+            self._comm = torch.cuda.Stream(device=g.device)
+        self._comm.wait_stream(g.stream)
+        stack = contextlib.ExitStack()
+        stack.enter_context(g._on())
+        stack.enter_context(torch.cuda.stream(self._comm))
+        return stack
+
+    def comm_fence(self):
+        """The next launch reads the received halo rows: main waits comm."""
+        self.grid.stream.wait_stream(self._comm)
 
     def layers(self, buf, first, count):
         f = self.grid.fields[buf]

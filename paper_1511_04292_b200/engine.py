@@ -242,6 +242,41 @@ class DeviceGrid:
                 ctypes.byref(out), self._sp), "srj_plan_run")
         return (src, a, b)[out.value]
 
+    def sub_plan(self, own_lo, own_hi):
+        """A plan over the same fields that relaxes, stores and counts only
+        local rows [own_lo, own_hi) (cached; the slab solver's edge / inner
+        launches).  Rows outside the range are read, never written."""
+        key = (int(own_lo), int(own_hi))
+        plans = self.__dict__.setdefault("_sub_plans", {})
+        if key not in plans:
+            desc = _lib.SrjPlanDesc()
+            ctypes.memmove(ctypes.byref(desc), ctypes.byref(self.desc), ctypes.sizeof(desc))
+            desc.own0_begin, desc.own0_end = key
+            plan = ctypes.c_void_p()
+            with self._on():
+                _lib.check(self.lib.srj_plan_create(ctypes.byref(desc), ctypes.byref(plan)),
+                           "srj_plan_create")
+            plans[key] = plan
+        return plans[key]
+
+    def run_single(self, plan, src, dst, weights, first, nsteps, norms):
+        """One fused launch of ``plan``: buffer ``src`` -> buffer ``dst``
+        (nsteps <= the plan's fused depth), per-step norms into the device
+        tensor ``norms`` (2 * nsteps doubles)."""
+        spare = [i for i in range(3) if i not in (src, dst)][0]
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        out = ctypes.c_int32(0)
+        f = self.fields
+        with self._on():
+            _lib.check(self.lib.srj_plan_run(
+                plan, ctypes.c_void_p(f[src].data_ptr()), ctypes.c_void_p(f[dst].data_ptr()),
+                ctypes.c_void_p(f[spare].data_ptr()),
+                w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(w), int(first),
+                int(nsteps), int(nsteps), ctypes.c_void_p(norms.data_ptr()), ctypes.byref(out),
+                self._sp), "srj_plan_run")
+        if out.value != 1:
+            raise RuntimeError("expected a single fused launch (fuse >= nsteps)")
+
     def gs(self, idx, omega, nsweeps):
         """``nsweeps`` in-place Gauss-Seidel / SOR sweeps of field buffer
         ``idx`` (srj_plan_gs); per-sweep (dmax, rmax) land in ``self.norms``."""
@@ -266,9 +301,13 @@ class DeviceGrid:
         return float(v[0]), float(v[1])
 
     def close(self):
-        if getattr(self, "plan", None) is not None:
+        subs = self.__dict__.pop("_sub_plans", {})
+        if subs or getattr(self, "plan", None) is not None:
             with self._on():
-                self.lib.srj_plan_destroy(self.plan)
+                for plan in subs.values():
+                    self.lib.srj_plan_destroy(plan)
+                if getattr(self, "plan", None) is not None:
+                    self.lib.srj_plan_destroy(self.plan)
             self.plan = None
 
     def __del__(self):

@@ -48,19 +48,38 @@ class OracleSlab:
         k = fields.get("kappa")
         self.kappa = None if k is None else np.ascontiguousarray(sl(k))
         self.own = d.own_local
+        self.first_part = d.row_parts()[0][0]
         self.normbuf = torch.zeros(2)
 
     def reserve(self, n):
         self.normbuf = torch.zeros(2 * n, dtype=torch.float64)
 
-    def run(self, src, dst, weights, first, nsteps, off):
-        self.bufs[dst][...] = self.bufs[src]
+    def run(self, src, dst, weights, first, nsteps, off, rows=None):
+        if rows is None:
+            self.bufs[dst][...] = self.bufs[src]
+            work, own = self.bufs[dst], self.own
+        else:  # edge / inner part: relax a copy, store only rows [a, b)
+            work, own = self.bufs[src].copy(), rows
         for s in range(nsteps):
-            p = _P(self.bufs[dst], self.src, self.c, self.lo, self.hi)
+            p = _P(work, self.src, self.c, self.lo, self.hi)
             w = weights[(first + s) % len(weights)]
-            dm, rm = oracle.np_step(p, w, kappa=self.kappa, own_rows=self.own)
-            self.normbuf[2 * (off + s)] = dm
-            self.normbuf[2 * (off + s) + 1] = rm
+            dm, rm = oracle.np_step(p, w, kappa=self.kappa, own_rows=own)
+            i = 2 * (off + s)
+            if rows is not None and rows != self.first_part:
+                dm, rm = max(dm, float(self.normbuf[i])), max(rm, float(self.normbuf[i + 1]))
+            self.normbuf[i] = dm
+            self.normbuf[i + 1] = rm
+        if rows is not None:
+            a, b = rows
+            self.bufs[dst][1 + a:1 + b] = work[1 + a:1 + b]
+
+    def comm(self):
+        import contextlib
+
+        return contextlib.nullcontext()
+
+    def comm_fence(self):
+        pass
 
     def layers(self, buf, first, count):
         return torch.from_numpy(self.bufs[buf][first:first + count])
@@ -75,13 +94,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, case, out_q):
+def _worker(rank, world, port, case, out_q, overlap=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         fields, w, steps, fuse = case()
         d = SlabDecomposition(fields["source"].shape[0], world, rank, halo=fuse)
-        solver = SlabSolver(OracleSlab(fields, d), d, fuse=fuse)
+        solver = SlabSolver(OracleSlab(fields, d), d, fuse=fuse, overlap=overlap)
+        assert solver.overlap == (world > 1 and overlap is not False)
         cur, allnorms, done = 0, [], 0
         for chunk in (steps // 3, steps - steps // 3):  # two chunks, snapshot rotation
             cur, norms = solver.run(cur, w, done, chunk)
@@ -121,13 +141,17 @@ def reference(case):
     return p.u, norms
 
 
+@pytest.mark.parametrize("overlap", [None, False])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("case", [case_2d, case_3d, case_nl])
-def test_slab_solver_matches_single_process(world, case):
+def test_slab_solver_matches_single_process(world, case, overlap):
+    """overlap=None: the default edge / inner split with the exchange posted
+    between the two (SlabSolver.overlap); False: one launch then exchange."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, overlap))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = sorted(q.get(timeout=240) for _ in range(world))
@@ -149,3 +173,11 @@ def test_decomposition_ranges():
     assert d[1].recvs() == [(0, 1, 2), (2, 6, 2)]
     with pytest.raises(ValueError):
         SlabDecomposition(5, 3, 0, halo=2)
+    # edge / inner split (local interior rows)
+    assert d[0].row_parts() == ([(2, 4)], (0, 2))
+    assert d[1].row_parts() == ([(2, 5)], None)  # thinner than two halos: all edge
+    assert d[2].row_parts() == ([(2, 4)], (4, 5))
+    e = [SlabDecomposition(40, 3, r, halo=3) for r in range(3)]
+    assert e[0].row_parts() == ([(11, 14)], (0, 11))
+    assert e[1].row_parts() == ([(3, 6), (13, 16)], (6, 13))
+    assert e[2].row_parts() == ([(3, 6)], (6, 16))

@@ -10,6 +10,8 @@ put the boundary columns at every lane/cell position of the edge bands and
 include grids of one band and of few rows.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -109,7 +111,7 @@ def test_default_fuse_neumann_laplace_matches_one_sweep_per_launch():
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SRJ_BC_RANDOM_CASES", "16"))))
 def test_random_fused_faces(seed):
     """Random shapes (band-kernel sizes), face kinds, scalar or per-position
     face values, fused depth 2..4 and coefficient mode."""

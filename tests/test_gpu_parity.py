@@ -284,13 +284,14 @@ class _EmulatedRanks:
     (no kernels wait on each other; the NCCL path is covered by the gloo tests
     in test_distributed.py with the same SlabDecomposition plan)."""
 
-    def __init__(self, fields, world, fuse):
+    def __init__(self, fields, world, fuse, split=False):
         from paper_1511_04292_b200.distributed import DeviceSlab, SlabDecomposition
 
         n0 = fields["source"].shape[0]
         self.d = [SlabDecomposition(n0, world, r, halo=fuse) for r in range(world)]
         self.b = [DeviceSlab(fields, d) for d in self.d]
         self.fuse = fuse
+        self.split = split  # SlabSolver.overlap: edge launches, exchange on comm, inner
 
     def run(self, w, nsteps):
         import torch
@@ -302,13 +303,28 @@ class _EmulatedRanks:
         while k < nsteps:
             t = min(self.fuse, nsteps - k)
             dst = others[flip]
-            for b in self.b:
-                b.run(cur, dst, w, k, t, k)
+            parts = [d.row_parts() for d in self.d]
+            for b, (edges, _) in zip(self.b, parts):
+                if not self.split:
+                    b.run(cur, dst, w, k, t, k)
+                for rows in edges if self.split else ():
+                    b.run(cur, dst, w, k, t, k, rows=rows)
             for r, d in enumerate(self.d):  # rank r receives from its neighbours
                 for peer, first, count in d.recvs():
                     src_first = [s for s in self.d[peer].sends() if s[0] == r][0][1]
-                    self.b[r].layers(dst, first, count).copy_(
-                        self.b[peer].layers(dst, src_first, count))
+                    if self.split:  # on the receiver's comm stream, after both edges
+                        self.b[r].grid.stream.wait_stream(self.b[peer].grid.stream)
+                        with self.b[r].comm():
+                            self.b[r].layers(dst, first, count).copy_(
+                                self.b[peer].layers(dst, src_first, count))
+                    else:
+                        self.b[r].layers(dst, first, count).copy_(
+                            self.b[peer].layers(dst, src_first, count))
+            if self.split:
+                for b, (_, inner) in zip(self.b, parts):
+                    if inner is not None:
+                        b.run(cur, dst, w, k, t, k, rows=inner)
+                    b.comm_fence()
             cur, flip, k = dst, 1 - flip, k + t
         torch.cuda.synchronize()
         norms = np.max([b.norms(nsteps).cpu().numpy() for b in self.b], axis=0)
@@ -316,12 +332,15 @@ class _EmulatedRanks:
         return field, norms.reshape(nsteps, 2)
 
 
-@pytest.mark.parametrize("world,fuse", [(2, 4), (4, 3), (3, 1)])
-def test_slab_decomposition_bitwise_on_one_gpu(table, world, fuse):
-    """k-rank slab solve == single-GPU solve bit for bit (cfg2 recipe)."""
+@pytest.mark.parametrize("split", [False, True])
+@pytest.mark.parametrize("world,fuse", [(2, 4), (4, 3), (3, 1), (40, 4)])
+def test_slab_decomposition_bitwise_on_one_gpu(table, world, fuse, split):
+    """k-rank slab solve == single-GPU solve bit for bit (cfg2 recipe);
+    split: the overlapped schedule (edge rows, exchange, inner rows, each part
+    its own plan, norms folded); 40 ranks make slabs thinner than two halos."""
     f = config_fields("cfg2", (331, 270))
     w = quantize(table.lookup(6, 4096)).weight_sequence
-    ranks = _EmulatedRanks(f, world, fuse)
+    ranks = _EmulatedRanks(f, world, fuse, split)
     field, norms = ranks.run(w, 97)
     p = problem_from(f)
     hist, _ = run_steps(p, w, 97, fuse=fuse)
@@ -329,11 +348,12 @@ def test_slab_decomposition_bitwise_on_one_gpu(table, world, fuse):
     assert np.array_equal(norms[:, 1], hist.true_residual_inf)
 
 
+@pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("fuse", [1, 2])
-def test_slab_decomposition_3d_on_one_gpu(table, fuse):
+def test_slab_decomposition_3d_on_one_gpu(table, fuse, split):
     f = config_fields("cfg3", (37, 30, 66))
     w = quantize(table.lookup(10, 512)).weight_sequence
-    field, norms = _EmulatedRanks(f, 3, fuse).run(w, 40)
+    field, norms = _EmulatedRanks(f, 3, fuse, split).run(w, 40)
     p = problem_from(f)
     hist, _ = run_steps(p, w, 40, fuse=1)
     assert np.array_equal(field, p.interior)

@@ -26,21 +26,23 @@ def fields(shape, masked, seed=0):
     return (np.zeros(tuple(n + 2 for n in shape)), rng.standard_normal(shape), c, lo, hi, mask)
 
 
+FUSE = [int(x) for x in os.environ.get("VAR_FUSE", "1").split(",")]
 for shape, bpu in (((4096, 4096), 65), ((512, 512, 512), 81)):
+  for fuse in (FUSE if len(shape) == 2 else [1]):
     for masked in (False, True):
         u, s, c, lo, hi, mask = fields(shape, masked)
         dev = DeviceGrid(u, s, c, lo, hi, active=mask)
         w = np.array([1.3, 0.7])
-        dev.run(0, w, 0, 8, 1)
+        dev.run(0, w, 0, 8, fuse)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         steps = 40
         e0.record(dev.stream)
-        dev.run(0, w, 0, steps, 1)
+        dev.run(0, w, 0, steps, fuse)
         e1.record(dev.stream)
         torch.cuda.synchronize()
         g = np.prod(shape) * steps / (e0.elapsed_time(e1) * 1e-3) / 1e9
         b = bpu if masked else bpu - 1
-        print(json.dumps({"shape": shape, "masked": masked, "glups": round(g, 1),
+        print(json.dumps({"shape": shape, "fuse": fuse, "masked": masked, "glups": round(g, 1),
                           "bytes_per_update": b, "frac": round(g * b / PEAK, 3)}), flush=True)
         dev.close()
