@@ -126,10 +126,10 @@ typedef struct {
                                     FIXED everywhere.  Non-FIXED faces refresh
                                     the ghosts after every launch (BoundaryRule,
                                     grids.py:73-112, refresh_ghosts :225-247);
-                                    2D MIRROR / FACE_DIRICHLET faces fuse up to
-                                    4 sweeps per launch (the ghosts between
-                                    fused sweeps are formed on chip), PERIODIC
-                                    and 3D run one sweep per launch;
+                                    MIRROR / FACE_DIRICHLET faces keep fusing
+                                    sweeps (2D up to 4, 3D up to 3; the ghosts
+                                    between fused sweeps are formed on chip),
+                                    PERIODIC runs one sweep per launch;
                                     single-slab only */
 } srj_plan_desc;
 

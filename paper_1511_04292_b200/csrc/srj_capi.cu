@@ -330,27 +330,27 @@ struct Kernel3DTB {
   int tj, tk, box_cols, box_rows;
 };
 
-template <int T, bool NL, bool RECIP>
+template <int T, bool NL, bool RECIP, bool BCF = false>
 struct K3TB {
   using B = Tile3D<T>;
   static void configure() {
     static std::atomic<uint64_t> done{0};
     once_per_device(done, [] {
-      cudaFuncSetAttribute(sweep3d_tb<T, NL, RECIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(sweep3d_tb<T, NL, RECIP, BCF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(B::smem_bytes()));
     });
   }
   static void launch(const Sweep3DTBParams &p, const CUtensorMap &tu, const CUtensorMap &tf,
                      int blocks, cudaStream_t s) {
     configure();
-    sweep3d_tb<T, NL, RECIP><<<blocks, B::THREADS, B::smem_bytes(), s>>>(p, tu, tf);
+    sweep3d_tb<T, NL, RECIP, BCF><<<blocks, B::THREADS, B::smem_bytes(), s>>>(p, tu, tf);
   }
   static int bps() {
     static std::atomic<int> cache[kMaxDevices];
     return cached_per_device(cache, [] {
       configure();
       int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d_tb<T, NL, RECIP>, B::THREADS,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d_tb<T, NL, RECIP, BCF>, B::THREADS,
                                                     B::smem_bytes());
       return n > 0 ? n : 1;
     });
@@ -359,15 +359,19 @@ struct K3TB {
 };
 
 template <int T>
-Kernel3DTB pick3d_tb_t(bool nl, bool recip) {
+Kernel3DTB pick3d_tb_t(bool nl, bool recip, bool bcf) {
+  if (bcf) {
+    if (recip) return nl ? K3TB<T, true, true, true>::get() : K3TB<T, false, true, true>::get();
+    return nl ? K3TB<T, true, false, true>::get() : K3TB<T, false, false, true>::get();
+  }
   if (recip) return nl ? K3TB<T, true, true>::get() : K3TB<T, false, true>::get();
   return nl ? K3TB<T, true, false>::get() : K3TB<T, false, false>::get();
 }
 
-Kernel3DTB pick3d_tb(int T, bool nl, bool recip) {
+Kernel3DTB pick3d_tb(int T, bool nl, bool recip, bool bcf) {
   switch (T) {
-    case 2: return pick3d_tb_t<2>(nl, recip);
-    default: return pick3d_tb_t<3>(nl, recip);
+    case 2: return pick3d_tb_t<2>(nl, recip, bcf);
+    default: return pick3d_tb_t<3>(nl, recip, bcf);
   }
 }
 
@@ -442,10 +446,10 @@ __global__ void selftest_div(const double *a, int64_t n, double c, double y, dou
 struct srj_plan {
   srj_plan_desc d;
   bool has_bc;       // some face is not FIXED: refresh ghosts after each launch
-  bool bc_fusable;   // ...and all of them are MIRROR/FACE_DIRICHLET on a 2D grid
+  bool bc_fusable;   // ...and none is PERIODIC: fused launches form the ghosts on chip
   int default_fuse;
   double *partials;  // [kResidBlocks][2] device scratch
-  double *bc_scalars;  // [2][2] device copies of the 2D faces' scalar values (fused BCs)
+  double *bc_scalars;  // [3][2] device copies of the faces' scalar values (fused BCs)
   // small-grid cluster path: per-chunk omegas (device + pinned staging)
   double *d_omegas = nullptr, *h_omegas = nullptr;
   int64_t omega_cap = 0;
@@ -593,9 +597,10 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
     return fail(SRJ_EUNSUPPORTED, "non-FIXED boundary rules need the whole grid on one plan");
   }
   // non-FIXED ghosts change every step.  MIRROR and FACE_DIRICHLET ghosts are a
-  // function of the adjacent cell, so the 2D band kernel folds them into its
-  // fused stages; PERIODIC (the opposite face) and 3D run one sweep per launch
-  p->bc_fusable = p->has_bc && l.ndim == 2;
+  // function of the adjacent cell, so the 2D band kernel and the 3D tile
+  // kernel fold them into their fused stages; PERIODIC (the opposite face)
+  // runs one sweep per launch
+  p->bc_fusable = p->has_bc;
   for (int a = 0; a < l.ndim; ++a)
     if (desc->bc[a][0].kind == SRJ_BC_PERIODIC) p->bc_fusable = false;
   p->default_fuse = (desc->coef_mode == 0 && (!p->has_bc || p->bc_fusable))
@@ -609,8 +614,8 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
     return cuda_fail(e, "cudaMalloc(partials)");
   }
   if (p->bc_fusable) {
-    double v[4];
-    for (int f = 0; f < 4; ++f) v[f] = desc->bc[f >> 1][f & 1].value;
+    double v[6];
+    for (int f = 0; f < 6; ++f) v[f] = desc->bc[f >> 1][f & 1].value;
     e = cudaMalloc(&p->bc_scalars, sizeof(v));
     if (e == cudaSuccess) e = cudaMemcpy(p->bc_scalars, v, sizeof(v), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
@@ -979,7 +984,15 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
       p.tma_row0 = l.halo0 * p.rows_per_plane + 1;  // row of (i=0, j=0)
       for (int q = 0; q < t; ++q) p.omega[q] = weights[(first + k + q) % m];
       p.norms = d_norms + 2 * k;
-      const Kernel3DTB k3 = pick3d_tb(t, nl, p.kinv != 0.0);
+      for (int a = 0; a < 3; ++a)
+        for (int side = 0; side < 2; ++side) {
+          const srj_face_rule &b = d.bc[a][side];
+          p.bc_kind[a][side] = b.kind;
+          const bool arr = b.kind == SRJ_BC_FACE_DIRICHLET && b.values;
+          p.bc_ptr[a][side] = arr ? b.values : plan->bc_scalars + 2 * a + side;
+          p.bc_step[a][side] = arr ? 1 : 0;
+        }
+      const Kernel3DTB k3 = pick3d_tb(t, nl, p.kinv != 0.0, plan->has_bc);
       p.ntj = int((l.n[1] + k3.tj - 1) / k3.tj);
       p.ntk = int((l.n[2] + k3.tk - 1) / k3.tk);
       const long tiles = long(p.ntj) * p.ntk;

@@ -40,7 +40,22 @@ struct Sweep3DTBParams {
   int tma_row0;        // tensor row of interior (i=0, j=0)
   double omega[kMaxFuse];
   double *norms;       // [T][2]
+  // MIRROR / FACE_DIRICHLET faces under fusion (kernel flag BCF): stages
+  // 1..T-1 write, next to every boundary cell they relax, the ghost the
+  // per-sweep refresh would hold (so stage t+1 reads it from its window)
+  int bc_kind[3][2];           // SRJ_BC_* per (axis, side)
+  const double *bc_ptr[3][2];  // face_dirichlet value at face position q: bc_ptr[q * bc_step]
+  int bc_step[3][2];           // 1: per-position array; 0: the face's scalar
 };
+
+// The refreshed ghost next to boundary cell value adj at face position q
+// (ghost_refresh's arithmetic, srj_reduce.cuh).
+__device__ __forceinline__ double bc_ghost3(const Sweep3DTBParams &p, int ax, int side,
+                                            double adj, int64_t q) {
+  if (p.bc_kind[ax][side] == 1) return adj;
+  const double v = __ldg(p.bc_ptr[ax][side] + q * p.bc_step[ax][side]);
+  return __dsub_rn(__dmul_rn(2.0, v), adj);
+}
 
 template <int T>
 struct Tile3D {
@@ -63,7 +78,7 @@ struct Tile3D {
   static constexpr int MINB = (smem_bytes() + 1024) * 2 <= 233472 ? 2 : 1;
 };
 
-template <int T, bool NL, bool RECIP>
+template <int T, bool NL, bool RECIP, bool BCF>
 __global__ void __launch_bounds__(Tile3D<T>::THREADS, Tile3D<T>::MINB)
     sweep3d_tb(const __grid_constant__ Sweep3DTBParams p, const __grid_constant__ CUtensorMap tm_u,
                 const __grid_constant__ CUtensorMap tm_f) {
@@ -145,6 +160,34 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, Tile3D<T>::MINB)
     }
   }
 
+  // BCF, stages 1..T-1, 8 bits per slot: bit 0 = in-plane ghost cell whose
+  // value the adjacent boundary cell's thread writes (skip the passthrough);
+  // bits 1-4 = boundary cell writing its j-1 / j+1 / k-1 / k+1 ghost
+  uint64_t bcm[T];
+#pragma unroll
+  for (int t = 1; t <= T; ++t) {
+    bcm[t - 1] = 0;
+    if (!BCF || t == T) continue;
+    const int RK = HK - 2 * t, NC = (HJ - 2 * t) * RK;
+#pragma unroll
+    for (int u = 0; u < UM; ++u) {
+      const int q = tid + u * B::THREADS;
+      if (q >= NC) continue;
+      const int j = j0 + t + q / RK, k = k0 + t + q % RK;
+      const bool jin = j >= 0 && j < p.n1, kin = k >= 0 && k < p.n2;
+      unsigned b = 0;
+      if (kin && ((j == -1 && p.bc_kind[1][0]) || (j == p.n1 && p.bc_kind[1][1]))) b |= 1u;
+      if (jin && ((k == -1 && p.bc_kind[2][0]) || (k == p.n2 && p.bc_kind[2][1]))) b |= 1u;
+      if (jin && kin) {
+        if (j == 0 && p.bc_kind[1][0]) b |= 2u;
+        if (j == p.n1 - 1 && p.bc_kind[1][1]) b |= 4u;
+        if (k == 0 && p.bc_kind[2][0]) b |= 8u;
+        if (k == p.n2 - 1 && p.bc_kind[2][1]) b |= 16u;
+      }
+      bcm[t - 1] |= uint64_t(b) << (8 * u);
+    }
+  }
+
   double rmx[T];
 #pragma unroll
   for (int t = 0; t < T; ++t) rmx[t] = 0.0;
@@ -213,12 +256,45 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, Tile3D<T>::MINB)
     for (int t = 1; t <= T; ++t) {
       const int pl = rho - 2 * t + 1;
       const bool own_plane = pl >= i0 && pl < i1;
+      const bool pin = pl >= 0 && pl < p.n0;
+      // (BCF) a plane-face tick of this stage: every cell takes the general
+      // write path; otherwise only threads holding boundary / ghost cells
+      const bool plane_fix =
+          BCF && ((pl == 0 && p.bc_kind[0][0]) || (pl == p.n0 && p.bc_kind[0][1]));
       double *out = (t < T) ? win + (t - 1) * NW * TILE + (pl & (NW - 1)) * TILE : nullptr;
 #pragma unroll
       for (int u = 0; u < UM; ++u) {
         const int o = off[t - 1][u];
         if (o < 0) continue;
-        if (t < T) {
+        if (t < T && BCF && (plane_fix || (pin && bcm[t - 1] != 0))) {
+          // ghosts of this stage's output for stage t+1 (see bcm above);
+          // plane faces: plane -1 is written when plane 0 is relaxed (two
+          // ticks before stage t+1 reads it), plane n0 when it passes through
+          const bool inb = (flg[t - 1] >> u) & 1u;
+          const unsigned b = unsigned(bcm[t - 1] >> (8 * u)) & 0xffu;
+          double v = y[t - 1][u];
+          const bool lo_pl = pl == 0 && p.bc_kind[0][0] && inb;
+          const bool hi_pl = pl == p.n0 && p.bc_kind[0][1] && inb;
+          if (lo_pl || hi_pl || (pin && b > 1u)) {
+            const int q = tid + u * B::THREADS, RK = HK - 2 * t;
+            const int j = j0 + t + q / RK, k = k0 + t + q % RK;
+            const double *wt = win + (t - 1) * NW * TILE;
+            if (hi_pl)
+              v = bc_ghost3(p, 0, 1, wt[((p.n0 - 1) & (NW - 1)) * TILE + o],
+                            int64_t(j) * p.n2 + k);
+            if (lo_pl)
+              win[(t - 1) * NW * TILE + ((-1) & (NW - 1)) * TILE + o] =
+                  bc_ghost3(p, 0, 0, v, int64_t(j) * p.n2 + k);
+            if (pin && b > 1u) {
+              const int64_t qj = int64_t(pl) * p.n2 + k, qk = int64_t(pl) * p.n1 + j;
+              if (b & 2u) out[o - HS] = bc_ghost3(p, 1, 0, v, qj);
+              if (b & 4u) out[o + HS] = bc_ghost3(p, 1, 1, v, qj);
+              if (b & 8u) out[o - 1] = bc_ghost3(p, 2, 0, v, qk);
+              if (b & 16u) out[o + 1] = bc_ghost3(p, 2, 1, v, qk);
+            }
+          }
+          if (!(pin && (b & 1u))) out[o] = v;
+        } else if (t < T) {
           out[o] = y[t - 1][u];
         } else if (own_plane && ((flg[t - 1] >> (8 + u)) & 1u)) {
           p.dst[int64_t(pl) * p.plane + goff[u]] = y[t - 1][u];

@@ -8,9 +8,9 @@ module's look-alikes: any object with the ``GridProblem`` attributes
 ``_active``, ``post_sweep``) and any cycle with ``weight_sequence``.
 
 GPU scope: 2-D 5-point and 3-D 7-point stencils with
-every reference boundary rule (FIXED ghosts, and 2-D mirror / face-Dirichlet
-faces, run fused multi-sweep kernels; periodic faces and 3-D non-FIXED faces
-run one sweep per launch; a device ghost refresh follows every launch),
+every reference boundary rule (FIXED, mirror and face-Dirichlet faces run
+fused multi-sweep kernels; periodic faces run one sweep per launch; a device
+ghost refresh follows every launch),
 constant or per-cell coefficients, optional mask,
 optional nonlinear source, ``post_sweep`` hooks that copy field values (e.g.
 the spherical ``tie_origin``; applied on the device as a gather after every

@@ -1,4 +1,4 @@
-"""Fused multi-sweep launches with MIRROR / FACE_DIRICHLET faces (2D).
+"""Fused multi-sweep launches with MIRROR / FACE_DIRICHLET faces (2D, 3D).
 
 The band kernel relaxes stages 2..T of a launch against the ghost the
 reference refreshes after every sweep (grids.py:225-247), computed from the
@@ -7,7 +7,8 @@ once per launch.  Each case is compared bit for bit with the oracle's
 step-by-step sweep + refresh (``oracle.run_bc``).  Grids are above the
 small-grid cluster threshold (2^18 cells) so the band kernel runs; the shapes
 put the boundary columns at every lane/cell position of the edge bands and
-include grids of one band and of few rows.
+include grids of one band and of few rows.  3D: the CTA-tile kernel (T=2, 3)
+writes each boundary cell's ghost into the next stage's window.
 """
 
 import os
@@ -26,18 +27,19 @@ W = np.array([7.3, 0.61, 0.93, 0.55, 0.97, 0.72, 0.88, 0.51, 0.99])
 
 def _fields(shape, seed, var=False, masked=False):
     rng = np.random.default_rng(seed)
+    nd = len(shape)
     f = {"u": rng.standard_normal(tuple(n + 2 for n in shape)),
          "source": rng.standard_normal(shape), "mask": None}
     if var:
-        f["center"] = 4.0 + rng.random(shape)
-        f["lower"] = tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(2))
-        f["upper"] = tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(2))
+        f["center"] = 2.0 * nd + rng.random(shape)
+        f["lower"] = tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd))
+        f["upper"] = tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd))
         if masked:
             f["mask"] = rng.random(shape) > 0.1
     else:
-        f["center"] = np.full(shape, 4.0)
-        f["lower"] = tuple(np.full(shape, -1.0) for _ in range(2))
-        f["upper"] = tuple(np.full(shape, -1.0) for _ in range(2))
+        f["center"] = np.full(shape, 2.0 * nd)
+        f["lower"] = tuple(np.full(shape, -1.0) for _ in range(nd))
+        f["upper"] = tuple(np.full(shape, -1.0) for _ in range(nd))
     return f
 
 
@@ -133,3 +135,19 @@ def test_random_fused_faces(seed):
     var = bool(rng.random() < 0.3)
     _run((n0, n1), tuple(bc), int(rng.integers(2, 5)), int(rng.integers(3, 20)), seed=900 + seed,
          var=var, masked=var and bool(rng.random() < 0.5))
+
+
+CASES_3D = [
+    ((37, 30, 70), (((M, None), (M, None)), ((M, None), (M, None)), ((M, None), (M, None)))),
+    ((29, 26, 131), (((F, 0.5), (F, _vals((26, 131), 6))), ((M, None), (F, _vals((29, 131), 7))),
+                     ((F, _vals((29, 26), 8)), (X, None)))),
+    ((45, 13, 66), (((X, None), (M, None)), ((F, -1.0), (X, None)), ((M, None), (F, 2.5)))),
+    ((12, 40, 9), (((M, None), (F, 0.25)), ((X, None), (M, None)), ((F, _vals((12, 40), 9)), (M, None)))),
+]
+
+
+@pytest.mark.parametrize("fuse", [2, 3])
+@pytest.mark.parametrize("case", range(len(CASES_3D)))
+def test_fused_faces_3d(case, fuse):
+    shape, bc = CASES_3D[case]
+    _run(shape, bc, fuse, 11, seed=300 + 10 * case + fuse)

@@ -57,12 +57,13 @@ def main():
     ap.add_argument("--nl", type=int, default=1)
     ap.add_argument("--bc", default="", help="2D faces: mirror | face_dirichlet (all four)")
     a = ap.parse_args()
-    bc = None
+    bc = bc3 = None
     if a.bc:
         from paper_1511_04292_b200 import grids as G
 
         rule = G.MIRROR if a.bc == "mirror" else G.face_dirichlet(0.5)
         bc = ((rule, rule),) * 2
+        bc3 = ((rule, rule),) * 3
     tab = shipped_table()
     w = quantize(tab.lookup(6, 4096)).weight_sequence
     f = config_fields("cfg2", (a.n, a.n))
@@ -76,8 +77,8 @@ def main():
         f3 = config_fields("cfg3", (n, n, n))
         w3 = quantize(tab.lookup(10, 512)).weight_sequence
         for fuse3 in (1, 2, 3):
-            ms, g, frac = measure(f3, w3, 48, fuse3)
-            print(json.dumps(dict(kind="3d", n=n, fuse=fuse3, ms_per_sweep=ms, glups=g,
+            ms, g, frac = measure(f3, w3, 48, fuse3, bc=bc3)
+            print(json.dumps(dict(kind="3d" + ("-" + a.bc if a.bc else ""), n=n, fuse=fuse3, ms_per_sweep=ms, glups=g,
                                   frac_alg=frac)), flush=True)
     if not a.nl:
         return
