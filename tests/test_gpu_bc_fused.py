@@ -151,3 +151,25 @@ CASES_3D = [
 def test_fused_faces_3d(case, fuse):
     shape, bc = CASES_3D[case]
     _run(shape, bc, fuse, 11, seed=300 + 10 * case + fuse)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SRJ_BC_RANDOM_CASES", "16"))))
+def test_random_fused_faces_3d(seed):
+    """3D: random shapes (tile-edge positions along j and k), face kinds,
+    scalar or per-position face values, fused depth 2..3."""
+    rng = np.random.default_rng(700 + seed)
+    shape = tuple(int(x) for x in (rng.integers(6, 40), rng.integers(3, 40), rng.integers(3, 150)))
+    bc = []
+    for ax in range(3):
+        other = tuple(n for a, n in enumerate(shape) if a != ax)
+        pair = []
+        for _ in range(2):
+            k = ("fixed", "mirror", "face_dirichlet")[int(rng.integers(0, 3))]
+            v = None
+            if k == "face_dirichlet":
+                v = rng.standard_normal(other) if rng.random() < 0.5 else float(rng.standard_normal())
+            pair.append((k, v))
+        bc.append(tuple(pair))
+    if all(k == "fixed" for pair in bc for k, _ in pair):
+        bc[2] = (("mirror", None), bc[2][1])
+    _run(shape, tuple(bc), int(rng.integers(2, 4)), int(rng.integers(3, 14)), seed=1900 + seed)
