@@ -44,7 +44,12 @@ struct GSParams {
   double *norms;             // [nsweeps][2]: (dmax, rmax)
 };
 
-constexpr int kGSPublish = 16;  // publish progress every 16 steps (the release is a full memory barrier)
+constexpr int kGSPublish = 16;
+constexpr int kGSPrefetch = 96;  // columns ahead for the L1 prefetch of a lane's rows
+
+__device__ __forceinline__ void prefetch_l1(const void *ptr) {
+  asm volatile("prefetch.global.L1 [%0];\n" ::"l"(ptr));
+}  // publish progress every 16 steps (the release is a full memory barrier)
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
   unsigned long long v;
@@ -240,6 +245,19 @@ __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams 
           if (lane == 0) st_release_u64(p.prog + s, base + d + 1);
         }
         if (d + kPF + 1 < W) load(d + kPF + 1, cur);
+        // the register ring covers L1/L2 latency only; the lane's own row and
+        // its source/coefficient rows stream from HBM (a 4096^2 field is
+        // larger than L2), so pull the line kGSPrefetch columns ahead into L1
+        // once per line (own rows only: they are written by this warp alone)
+        const int64_t jp = j + kGSPrefetch;
+        if ((jp & 15) == 0 && jp >= 0 && jp < p.ncols && row_ok) {
+          prefetch_l1(u + off + jp);
+          prefetch_l1(p.f + off + jp);
+          if (VAR) {
+#pragma unroll
+            for (int a = 0; a < 1 + 2 * ND; ++a) prefetch_l1(p.coef[a] + off + jp);
+          }
+        }
       }
     }
     const double rm = warp_max(fabs(rmx));
