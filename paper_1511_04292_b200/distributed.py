@@ -239,7 +239,8 @@ class DeviceSlab:
         self._part_norms = None
         self._comm = None
         edges, _ = decomp.row_parts()
-        self._first_part = edges[0]  # the overlapped solver runs the edges first
+        # the overlapped solver runs the edges first (a single rank has none)
+        self._first_part = edges[0] if edges else None
 
     def reserve(self, nsteps):
         torch = self.grid.torch

@@ -348,6 +348,22 @@ def test_slab_decomposition_bitwise_on_one_gpu(table, world, fuse, split):
     assert np.array_equal(norms[:, 1], hist.true_residual_inf)
 
 
+def test_slab_grid_single_rank(table):
+    """SlabGrid at world size 1 (bench.py --slab at N=1): no neighbours, no
+    edge rows, same field as the plain solver."""
+    from paper_1511_04292_b200.distributed import SlabGrid
+
+    f = config_fields("cfg2", (300, 257))
+    w = quantize(table.lookup(6, 4096)).weight_sequence
+    g = SlabGrid(f, 0, 1, fuse=4)
+    cur = g.run(0, w, 0, 41)
+    field = g.backend.download_owned(cur)
+    p = problem_from(f)
+    hist, _ = run_steps(p, w, 41, fuse=4)
+    assert np.array_equal(field, p.interior)
+    assert np.array_equal(g.norms.numpy().reshape(-1, 2)[:, 1], hist.true_residual_inf)
+
+
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("fuse", [1, 2])
 def test_slab_decomposition_3d_on_one_gpu(table, fuse, split):
