@@ -330,7 +330,7 @@ struct Kernel3DTB {
   int tj, tk, box_cols, box_rows;
 };
 
-template <int T, bool NL, bool RECIP, bool BCF = false>
+template <int T, bool NL, bool RECIP, int BCF = 0>
 struct K3TB {
   using B = Tile3D<T>;
   static void configure() {
@@ -358,17 +358,22 @@ struct K3TB {
   static Kernel3DTB get() { return Kernel3DTB{launch, bps, B::TJ, B::TK, B::HS, B::HJ}; }
 };
 
+template <int T, int BCF>
+Kernel3DTB pick3d_tb_bc(bool nl, bool recip) {
+  if (recip) return nl ? K3TB<T, true, true, BCF>::get() : K3TB<T, false, true, BCF>::get();
+  return nl ? K3TB<T, true, false, BCF>::get() : K3TB<T, false, false, BCF>::get();
+}
+
+// bcf: 0 = FIXED faces; 1 = fused MIRROR / FACE_DIRICHLET faces; 2 = MIRROR only
 template <int T>
-Kernel3DTB pick3d_tb_t(bool nl, bool recip, bool bcf) {
-  if (bcf) {
-    if (recip) return nl ? K3TB<T, true, true, true>::get() : K3TB<T, false, true, true>::get();
-    return nl ? K3TB<T, true, false, true>::get() : K3TB<T, false, false, true>::get();
-  }
+Kernel3DTB pick3d_tb_t(bool nl, bool recip, int bcf) {
+  if (bcf == 1) return pick3d_tb_bc<T, 1>(nl, recip);
+  if (bcf == 2) return pick3d_tb_bc<T, 2>(nl, recip);
   if (recip) return nl ? K3TB<T, true, true>::get() : K3TB<T, false, true>::get();
   return nl ? K3TB<T, true, false>::get() : K3TB<T, false, false>::get();
 }
 
-Kernel3DTB pick3d_tb(int T, bool nl, bool recip, bool bcf) {
+Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf) {
   switch (T) {
     case 2: return pick3d_tb_t<2>(nl, recip, bcf);
     default: return pick3d_tb_t<3>(nl, recip, bcf);
@@ -600,7 +605,7 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
   // function of the adjacent cell, so the 2D band kernel and the 3D tile
   // kernel fold them into their fused stages; PERIODIC (the opposite face)
   // runs one sweep per launch
-  p->bc_fusable = p->has_bc;
+  p->bc_fusable = p->has_bc && (l.ndim == 2 || (l.n[1] < (1 << 15) && l.n[2] < (1 << 16)));
   for (int a = 0; a < l.ndim; ++a)
     if (desc->bc[a][0].kind == SRJ_BC_PERIODIC) p->bc_fusable = false;
   p->default_fuse = (desc->coef_mode == 0 && (!p->has_bc || p->bc_fusable))
@@ -992,7 +997,14 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
           p.bc_ptr[a][side] = arr ? b.values : plan->bc_scalars + 2 * a + side;
           p.bc_step[a][side] = arr ? 1 : 0;
         }
-      const Kernel3DTB k3 = pick3d_tb(t, nl, p.kinv != 0.0, plan->has_bc);
+      int bcf = 0;
+      if (plan->has_bc) {
+        bcf = 2;
+        for (int a = 0; a < 3; ++a)
+          for (int side = 0; side < 2; ++side)
+            if (d.bc[a][side].kind == SRJ_BC_FACE_DIRICHLET) bcf = 1;
+      }
+      const Kernel3DTB k3 = pick3d_tb(t, nl, p.kinv != 0.0, bcf);
       p.ntj = int((l.n[1] + k3.tj - 1) / k3.tj);
       p.ntk = int((l.n[2] + k3.tk - 1) / k3.tk);
       const long tiles = long(p.ntj) * p.ntk;

@@ -21,6 +21,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "srj_device.cuh"
 
 namespace srj {
@@ -41,8 +43,8 @@ struct Sweep3DTBParams {
   double omega[kMaxFuse];
   double *norms;       // [T][2]
   // MIRROR / FACE_DIRICHLET faces under fusion (kernel flag BCF): stages
-  // 1..T-1 write, next to every boundary cell they relax, the ghost the
-  // per-sweep refresh would hold (so stage t+1 reads it from its window)
+  // 2..T relax every boundary cell against the ghost the per-sweep refresh
+  // would hold, computed from the cell's own (previous-stage) value
   int bc_kind[3][2];           // SRJ_BC_* per (axis, side)
   const double *bc_ptr[3][2];  // face_dirichlet value at face position q: bc_ptr[q * bc_step]
   int bc_step[3][2];           // 1: per-position array; 0: the face's scalar
@@ -50,11 +52,15 @@ struct Sweep3DTBParams {
 
 // The refreshed ghost next to boundary cell value adj at face position q
 // (ghost_refresh's arithmetic, srj_reduce.cuh).
+// BCF == 2: every non-FIXED face is MIRROR (the ghost is the cell itself);
+// BCF == 1: the general branch-free form.
+template <int BCF>
 __device__ __forceinline__ double bc_ghost3(const Sweep3DTBParams &p, int ax, int side,
                                             double adj, int64_t q) {
-  if (p.bc_kind[ax][side] == 1) return adj;
+  if (BCF == 2) return adj;
   const double v = __ldg(p.bc_ptr[ax][side] + q * p.bc_step[ax][side]);
-  return __dsub_rn(__dmul_rn(2.0, v), adj);
+  const double fd = __dsub_rn(__dmul_rn(2.0, v), adj);
+  return p.bc_kind[ax][side] == 1 ? adj : fd;
 }
 
 template <int T>
@@ -78,7 +84,7 @@ struct Tile3D {
   static constexpr int MINB = (smem_bytes() + 1024) * 2 <= 233472 ? 2 : 1;
 };
 
-template <int T, bool NL, bool RECIP, bool BCF>
+template <int T, bool NL, bool RECIP, int BCF>
 __global__ void __launch_bounds__(Tile3D<T>::THREADS, Tile3D<T>::MINB)
     sweep3d_tb(const __grid_constant__ Sweep3DTBParams p, const __grid_constant__ CUtensorMap tm_u,
                 const __grid_constant__ CUtensorMap tm_f) {
@@ -160,33 +166,35 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, Tile3D<T>::MINB)
     }
   }
 
-  // BCF, stages 1..T-1, 8 bits per slot: bit 0 = in-plane ghost cell whose
-  // value the adjacent boundary cell's thread writes (skip the passthrough);
-  // bits 1-4 = boundary cell writing its j-1 / j+1 / k-1 / k+1 ghost
-  uint64_t bcm[T];
+  // BCF, stages 2..T, 4 bits per slot: the cell is next to a non-FIXED j-1 /
+  // j+1 / k-1 / k+1 face (interior cells only); jk = packed (j, k) for the
+  // face-value index.  cta_faces: some cell of this tile has such a face.
+  unsigned fb[T];
+  int jk[T][UM];
+  bool cta_faces = false;
 #pragma unroll
   for (int t = 1; t <= T; ++t) {
-    bcm[t - 1] = 0;
-    if (!BCF || t == T) continue;
+    fb[t - 1] = 0;
+    if (!BCF || t == 1) continue;
     const int RK = HK - 2 * t, NC = (HJ - 2 * t) * RK;
 #pragma unroll
     for (int u = 0; u < UM; ++u) {
       const int q = tid + u * B::THREADS;
+      jk[t - 1][u] = 0;
       if (q >= NC) continue;
       const int j = j0 + t + q / RK, k = k0 + t + q % RK;
-      const bool jin = j >= 0 && j < p.n1, kin = k >= 0 && k < p.n2;
+      if (j < 0 || j >= p.n1 || k < 0 || k >= p.n2) continue;
+      jk[t - 1][u] = (j << 16) | k;  // host: n1 < 2^15, n2 < 2^16 under BCF
       unsigned b = 0;
-      if (kin && ((j == -1 && p.bc_kind[1][0]) || (j == p.n1 && p.bc_kind[1][1]))) b |= 1u;
-      if (jin && ((k == -1 && p.bc_kind[2][0]) || (k == p.n2 && p.bc_kind[2][1]))) b |= 1u;
-      if (jin && kin) {
-        if (j == 0 && p.bc_kind[1][0]) b |= 2u;
-        if (j == p.n1 - 1 && p.bc_kind[1][1]) b |= 4u;
-        if (k == 0 && p.bc_kind[2][0]) b |= 8u;
-        if (k == p.n2 - 1 && p.bc_kind[2][1]) b |= 16u;
-      }
-      bcm[t - 1] |= uint64_t(b) << (8 * u);
+      if (j == 0 && p.bc_kind[1][0]) b |= 1u;
+      if (j == p.n1 - 1 && p.bc_kind[1][1]) b |= 2u;
+      if (k == 0 && p.bc_kind[2][0]) b |= 4u;
+      if (k == p.n2 - 1 && p.bc_kind[2][1]) b |= 8u;
+      fb[t - 1] |= b << (4 * u);
     }
+    cta_faces |= fb[t - 1] != 0;
   }
+  if (BCF) cta_faces = __syncthreads_or(cta_faces);
 
   double rmx[T];
 #pragma unroll
@@ -199,48 +207,83 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, Tile3D<T>::MINB)
     mbar_wait(&bar_f[it % NSF], (it / NSF) & 1);
     bool bad = false;
     double y[T][UM], num[T][UM], uc[T][UM];
+    // SUBV: stages >= 2 substitute the ghosts of non-FIXED faces (tiles
+    // holding j/k boundary cells, and the ticks where a stage relaxes plane
+    // 0 or n0-1); every other tick runs the FIXED kernel's code
+    auto stages = [&](auto subc) {
+      constexpr bool SUBV = decltype(subc)::value;
 #pragma unroll
-    for (int t = 1; t <= T; ++t) {
-      const int pl = rho - 2 * t + 1;  // plane this stage relaxes
-      const double *dn, *md, *up;
-      if (t == 1) {
-        up = ring_u + ((it + 2 * NSU - 2) % NSU) * TILE;
-        md = ring_u + ((it + NSU - 1) % NSU) * TILE;
-        dn = ring_u + (it % NSU) * TILE;
-      } else {
-        const double *w = win + (t - 2) * NW * TILE;
-        up = w + ((pl - 1) & (NW - 1)) * TILE;
-        md = w + (pl & (NW - 1)) * TILE;
-        dn = w + ((pl + 1) & (NW - 1)) * TILE;
-      }
-      const double *fp = ring_f + ((it - 2 * t + 1 + 2 * NSF) % NSF) * TILE;
-      const unsigned pa = (pl >= 0 && pl < p.n0) ? 0xffu : 0u;
-      const unsigned po = (pl >= i0 && pl < i1) ? 0xffu : 0u;
-      const unsigned act_m = flg[t - 1] & pa;
-      const unsigned own_m = (flg[t - 1] >> 8) & pa & po;
-      const double om = p.omega[t - 1];
-#pragma unroll
-      for (int u = 0; u < UM; ++u) {
-        const int o = off[t - 1][u];
-        if (o < 0) continue;
-        uc[t - 1][u] = md[o];
-        const bool a = (act_m >> u) & 1u;
-        const double sv = NL ? nl_source(fp[o], uc[t - 1][u]) : fp[o];
-        const double rr = resid7(sv, p.kc[0], uc[t - 1][u], p.kc[1], up[o], p.kc[2], dn[o],
-                                 p.kc[3], md[o - HS], p.kc[4], md[o + HS], p.kc[5], md[o - 1],
-                                 p.kc[6], md[o + 1]);
-        num[t - 1][u] = __dmul_rn(om, rr);
-        double d;
-        if (RECIP) {
-          d = div_recip(num[t - 1][u], p.kc[0], p.kinv, p.kinv_lo);
-          bad |= a && recip_unsafe(num[t - 1][u]);
+      for (int t = 1; t <= T; ++t) {
+        const int pl = rho - 2 * t + 1;  // plane this stage relaxes
+        const double *dn, *md, *up;
+        if (t == 1) {
+          up = ring_u + ((it + 2 * NSU - 2) % NSU) * TILE;
+          md = ring_u + ((it + NSU - 1) % NSU) * TILE;
+          dn = ring_u + (it % NSU) * TILE;
         } else {
-          d = __ddiv_rn(num[t - 1][u], p.kc[0]);
+          const double *w = win + (t - 2) * NW * TILE;
+          up = w + ((pl - 1) & (NW - 1)) * TILE;
+          md = w + (pl & (NW - 1)) * TILE;
+          dn = w + ((pl + 1) & (NW - 1)) * TILE;
         }
-        y[t - 1][u] = a ? __dadd_rn(uc[t - 1][u], d) : uc[t - 1][u];
-        if ((own_m >> u) & 1u) acc_max(rmx[t - 1], rr);
+        const double *fp = ring_f + ((it - 2 * t + 1 + 2 * NSF) % NSF) * TILE;
+        const unsigned pa = (pl >= 0 && pl < p.n0) ? 0xffu : 0u;
+        const unsigned po = (pl >= i0 && pl < i1) ? 0xffu : 0u;
+        const unsigned act_m = flg[t - 1] & pa;
+        const unsigned own_m = (flg[t - 1] >> 8) & pa & po;
+        const double om = p.omega[t - 1];
+        const bool plo = SUBV && t >= 2 && pl == 0 && p.bc_kind[0][0];
+        const bool phi = SUBV && t >= 2 && pl == p.n0 - 1 && p.bc_kind[0][1];
+#pragma unroll
+        for (int u = 0; u < UM; ++u) {
+          const int o = off[t - 1][u];
+          if (o < 0) continue;
+          const double c0 = md[o];
+          uc[t - 1][u] = c0;
+          const bool a = (act_m >> u) & 1u;
+          double nu = up[o], nd = dn[o], njm = md[o - HS], njp = md[o + HS], nkm = md[o - 1],
+                 nkp = md[o + 1];
+          if (SUBV && t >= 2) {
+            const unsigned b = a ? (fb[t - 1] >> (4 * u)) & 15u : 0u;
+            const int j = jk[t - 1][u] >> 16, k = jk[t - 1][u] & 0xffff;
+            const int64_t qi = int64_t(j) * p.n2 + k, qj = int64_t(pl) * p.n2 + k,
+                          qk = int64_t(pl) * p.n1 + j;
+            if (plo && a) nu = bc_ghost3<BCF>(p, 0, 0, c0, qi);
+            if (phi && a) nd = bc_ghost3<BCF>(p, 0, 1, c0, qi);
+            if (b & 1u) njm = bc_ghost3<BCF>(p, 1, 0, c0, qj);
+            if (b & 2u) njp = bc_ghost3<BCF>(p, 1, 1, c0, qj);
+            if (b & 4u) nkm = bc_ghost3<BCF>(p, 2, 0, c0, qk);
+            if (b & 8u) nkp = bc_ghost3<BCF>(p, 2, 1, c0, qk);
+          }
+          const double sv = NL ? nl_source(fp[o], c0) : fp[o];
+          const double rr = resid7(sv, p.kc[0], c0, p.kc[1], nu, p.kc[2], nd, p.kc[3], njm,
+                                   p.kc[4], njp, p.kc[5], nkm, p.kc[6], nkp);
+          num[t - 1][u] = __dmul_rn(om, rr);
+          double d;
+          if (RECIP) {
+            d = div_recip(num[t - 1][u], p.kc[0], p.kinv, p.kinv_lo);
+            bad |= a && recip_unsafe(num[t - 1][u]);
+          } else {
+            d = __ddiv_rn(num[t - 1][u], p.kc[0]);
+          }
+          y[t - 1][u] = a ? __dadd_rn(c0, d) : c0;
+          if ((own_m >> u) & 1u) acc_max(rmx[t - 1], rr);
+        }
+      }
+    };
+    bool sub = false;
+    if (BCF) {
+      sub = cta_faces;
+#pragma unroll
+      for (int t = 2; t <= T; ++t) {
+        const int pl = rho - 2 * t + 1;
+        sub |= (pl == 0 && p.bc_kind[0][0]) || (pl == p.n0 - 1 && p.bc_kind[0][1]);
       }
     }
+    if (BCF && sub)
+      stages(std::integral_constant<bool, true>{});
+    else
+      stages(std::integral_constant<bool, false>{});
     if (RECIP && __any_sync(kFull, bad)) {
 #pragma unroll
       for (int t = 1; t <= T; ++t) {
@@ -256,45 +299,12 @@ __global__ void __launch_bounds__(Tile3D<T>::THREADS, Tile3D<T>::MINB)
     for (int t = 1; t <= T; ++t) {
       const int pl = rho - 2 * t + 1;
       const bool own_plane = pl >= i0 && pl < i1;
-      const bool pin = pl >= 0 && pl < p.n0;
-      // (BCF) a plane-face tick of this stage: every cell takes the general
-      // write path; otherwise only threads holding boundary / ghost cells
-      const bool plane_fix =
-          BCF && ((pl == 0 && p.bc_kind[0][0]) || (pl == p.n0 && p.bc_kind[0][1]));
       double *out = (t < T) ? win + (t - 1) * NW * TILE + (pl & (NW - 1)) * TILE : nullptr;
 #pragma unroll
       for (int u = 0; u < UM; ++u) {
         const int o = off[t - 1][u];
         if (o < 0) continue;
-        if (t < T && BCF && (plane_fix || (pin && bcm[t - 1] != 0))) {
-          // ghosts of this stage's output for stage t+1 (see bcm above);
-          // plane faces: plane -1 is written when plane 0 is relaxed (two
-          // ticks before stage t+1 reads it), plane n0 when it passes through
-          const bool inb = (flg[t - 1] >> u) & 1u;
-          const unsigned b = unsigned(bcm[t - 1] >> (8 * u)) & 0xffu;
-          double v = y[t - 1][u];
-          const bool lo_pl = pl == 0 && p.bc_kind[0][0] && inb;
-          const bool hi_pl = pl == p.n0 && p.bc_kind[0][1] && inb;
-          if (lo_pl || hi_pl || (pin && b > 1u)) {
-            const int q = tid + u * B::THREADS, RK = HK - 2 * t;
-            const int j = j0 + t + q / RK, k = k0 + t + q % RK;
-            const double *wt = win + (t - 1) * NW * TILE;
-            if (hi_pl)
-              v = bc_ghost3(p, 0, 1, wt[((p.n0 - 1) & (NW - 1)) * TILE + o],
-                            int64_t(j) * p.n2 + k);
-            if (lo_pl)
-              win[(t - 1) * NW * TILE + ((-1) & (NW - 1)) * TILE + o] =
-                  bc_ghost3(p, 0, 0, v, int64_t(j) * p.n2 + k);
-            if (pin && b > 1u) {
-              const int64_t qj = int64_t(pl) * p.n2 + k, qk = int64_t(pl) * p.n1 + j;
-              if (b & 2u) out[o - HS] = bc_ghost3(p, 1, 0, v, qj);
-              if (b & 4u) out[o + HS] = bc_ghost3(p, 1, 1, v, qj);
-              if (b & 8u) out[o - 1] = bc_ghost3(p, 2, 0, v, qk);
-              if (b & 16u) out[o + 1] = bc_ghost3(p, 2, 1, v, qk);
-            }
-          }
-          if (!(pin && (b & 1u))) out[o] = v;
-        } else if (t < T) {
+        if (t < T) {
           out[o] = y[t - 1][u];
         } else if (own_plane && ((flg[t - 1] >> (8 + u)) & 1u)) {
           p.dst[int64_t(pl) * p.plane + goff[u]] = y[t - 1][u];
