@@ -304,7 +304,10 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
     for (int v = 0; v < V; ++v)
       if (lane_col + v == p.n1 - 1 && p.bc_kind[1][1]) bcm |= 2u << v;
   }
-  const bool warp_sub = BCF && __any_sync(kFull, bcm != 0);
+  // every edge band takes the substituting path once any column face is
+  // non-FIXED (bcm = 0 lanes just select their own neighbours): two edge
+  // code paths live at once on an SM cost more (i-cache) than the selects
+  const bool warp_sub = BCF && (p.bc_kind[1][0] || p.bc_kind[1][1]);
   const int tma_col = p.tma_col0 + col_band;
   const int tma_row = p.tma_row0 + rho_b;
 

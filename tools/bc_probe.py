@@ -25,8 +25,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--steps", type=int, default=480)
+    ap.add_argument("--jacobi", action="store_true",
+                    help="weight 0.9 on every sweep (no partial-cycle growth: the SRJ cycle's "
+                         "large weights can drive a partial cycle to inf/NaN, whose cells take "
+                         "the IEEE-division fallback)")
     a = ap.parse_args()
     w = quantize(shipped_table().lookup(6, 4096)).weight_sequence
+    if a.jacobi:
+        import numpy as np
+
+        w = np.array([0.9])
     f = config_fields("cfg2", (a.n, a.n))
     F, M = G.FIXED, G.MIRROR
     cases = {"none": ((F, F), (F, F)), "rows": ((M, M), (F, F)), "cols": ((F, F), (M, M)),
