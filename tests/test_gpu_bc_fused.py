@@ -173,3 +173,18 @@ def test_random_fused_faces_3d(seed):
     if all(k == "fixed" for pair in bc for k, _ in pair):
         bc[2] = (("mirror", None), bc[2][1])
     _run(shape, tuple(bc), int(rng.integers(2, 4)), int(rng.integers(3, 14)), seed=1900 + seed)
+
+
+@pytest.mark.parametrize("shape", [(270000, 1), (140000, 2), (2, 140000), (1, 270000), (3, 90001)])
+def test_fused_faces_degenerate_2d(shape):
+    """One or two columns (both column faces on one lane / cell) and one or
+    two rows (both row faces in the same slow ticks), above the cluster-path
+    size so the band kernel runs, T=4."""
+    bc = (((M, None), (F, 0.5)), ((F, -1.5), (M, None)))
+    _run(shape, bc, 4, 9, seed=sum(shape))
+
+
+@pytest.mark.parametrize("shape", [(30, 1, 40), (20, 33, 1), (1, 25, 70), (2, 2, 2)])
+def test_fused_faces_degenerate_3d(shape):
+    bc = (((M, None), (F, 0.5)), ((F, -1.5), (M, None)), ((M, None), (F, 2.0)))
+    _run(shape, bc, 2, 7, seed=sum(shape))
