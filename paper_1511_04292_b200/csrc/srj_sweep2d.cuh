@@ -58,9 +58,10 @@ struct Sweep2DParams {
   int tma_row0;        // tensor-map row of interior row 0
   double omega[kMaxFuse];
   double *norms;       // [T][2]: (dmax, rmax) per fused step
-  // MIRROR / FACE_DIRICHLET faces under fusion (kernel flag BCF): between
-  // stages the window's ghost cells are set to the ghost the reference
-  // refreshes after every sweep, a pure function of the adjacent cell
+  // MIRROR / FACE_DIRICHLET faces under fusion (kernel flag BCF): stages 2..T
+  // see the ghost the reference refreshes after every sweep, a pure function
+  // of the adjacent cell -- substituted for column faces (stage2d, SUB),
+  // written into the stage windows for row faces (SRJ_BCFIX)
   int bc_kind[2][2];           // SRJ_BC_* per (axis, side)
   const double *bc_ptr[2][2];  // face_dirichlet value at face position q: bc_ptr[q * bc_step]
   int bc_step[2][2];           // 1: per-position array; 0: the face's scalar
@@ -93,7 +94,8 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, const double (&u
                                         const double (&mid)[V], const double (&down)[V],
                                         const double *frow, int r, double om, int lane_col,
                                         int i0, int i1, int own_c0, int own_c1, int f_lo,
-                                        int f_hi, unsigned colact, bool cnt, unsigned bcm, double (&y)[V],
+                                        int f_hi, unsigned colact, bool cnt, unsigned bcm,
+                                        double (&y)[V],
                                         double (&num)[V], double &rmx, double &dmx, bool &bad) {
   double fv[V];
 #pragma unroll
