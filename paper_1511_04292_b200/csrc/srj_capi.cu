@@ -718,9 +718,11 @@ static int launch_ghosts(const srj_plan_desc &d, double *u0, cudaStream_t st) {
     g.value[ax][side] = d.bc[ax][side].value;
     g.values[ax][side] = d.bc[ax][side].values;
   }
-  const int64_t total = g.face_start[2 * l.ndim];
-  const int blocks = int(std::min<int64_t>((total + 255) / 256, int64_t(sm_count()) * 4));
-  ghost_refresh<<<std::max(blocks, 1), 256, 0, st>>>(g);
+  int64_t biggest = 1;
+  for (int f = 0; f < 2 * l.ndim; ++f)
+    biggest = std::max<int64_t>(biggest, g.face_start[f + 1] - g.face_start[f]);
+  const int blocks = int(std::min<int64_t>((biggest + 255) / 256, int64_t(sm_count())));
+  ghost_refresh<<<dim3(std::max(blocks, 1), 2 * l.ndim), 256, 0, st>>>(g);
   SRJ_CUDA(cudaGetLastError());
   return SRJ_OK;
 }

@@ -129,38 +129,40 @@ struct GhostParams {
   int64_t face_start[7];  // prefix sums of face sizes over the 2*ndim faces
 };
 
+// One face per blockIdx.y (2*ndim faces); blocks stride over the face's
+// cells in C order of the other axes, 32-bit index math (faces are far below
+// 2^31 cells; int64 division per cell made this kernel 4x slower).
 __global__ void __launch_bounds__(256) ghost_refresh(const __grid_constant__ GhostParams p) {
-  const int nf = 2 * p.ndim;
-  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < p.face_start[nf];
-       q += int64_t(gridDim.x) * blockDim.x) {
-    int f = 0;
-    while (q >= p.face_start[f + 1]) ++f;
-    const int ax = f >> 1, side = f & 1;
-    const int kind = p.kind[ax][side];
-    if (kind == 0) continue;
-    int64_t rem = q - p.face_start[f];
-    // position along the other axes (C order, interior indices)
-    int64_t off = 0;
-    for (int a = p.ndim - 1; a >= 0; --a) {
-      if (a == ax) continue;
-      const int64_t idx = rem % p.n[a];
-      rem /= p.n[a];
-      off += idx * p.stride[a];
-    }
-    const int64_t sa = p.stride[ax];
-    const int64_t ghost = off + (side ? int64_t(p.n[ax]) : -1) * sa;
-    const int64_t adj = off + (side ? int64_t(p.n[ax] - 1) : 0) * sa;
+  const int f = blockIdx.y;
+  const int ax = f >> 1, side = f & 1;
+  const int kind = p.kind[ax][side];
+  if (kind == 0) return;
+  // the other axes: (a0 outer, a1 inner); 2D has only a1
+  const int a1 = (ax == p.ndim - 1) ? p.ndim - 2 : p.ndim - 1;
+  const int a0 = (p.ndim == 3) ? ((ax == 0) ? 1 : 0) : -1;
+  const int n1 = p.n[a1];
+  const int ncell = int(p.face_start[f + 1] - p.face_start[f]);
+  const int64_t sa = p.stride[ax];
+  const int64_t s1 = p.stride[a1], s0 = a0 >= 0 ? p.stride[a0] : 0;
+  const int64_t ghost_off = (side ? int64_t(p.n[ax]) : -1) * sa;
+  const int64_t adj_off = (side ? int64_t(p.n[ax] - 1) : 0) * sa;
+  const int64_t per_off = (side ? 0 : int64_t(p.n[ax] - 1)) * sa;  // periodic source
+  const double *vals = p.values[ax][side];
+  const double val = p.value[ax][side];
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < ncell; q += gridDim.x * blockDim.x) {
+    const int i0 = (a0 >= 0) ? q / n1 : 0;
+    const int i1 = q - i0 * n1;
+    const int64_t off = int64_t(i0) * s0 + int64_t(i1) * s1;
     double g;
     if (kind == 1) {
-      g = p.u[adj];
+      g = p.u[off + adj_off];
     } else if (kind == 2) {
-      g = p.u[off + (side ? 0 : int64_t(p.n[ax] - 1)) * sa];
+      g = p.u[off + per_off];
     } else {
-      const double v = p.values[ax][side] ? p.values[ax][side][q - p.face_start[f]]
-                                          : p.value[ax][side];
-      g = __dsub_rn(__dmul_rn(2.0, v), p.u[adj]);
+      const double v = vals ? vals[q] : val;
+      g = __dsub_rn(__dmul_rn(2.0, v), p.u[off + adj_off]);
     }
-    p.u[ghost] = g;
+    p.u[off + ghost_off] = g;
   }
 }
 
