@@ -181,3 +181,48 @@ def test_decomposition_ranges():
     assert e[0].row_parts() == ([(11, 14)], (0, 11))
     assert e[1].row_parts() == ([(3, 6), (13, 16)], (6, 13))
     assert e[2].row_parts() == ([(3, 6)], (6, 16))
+
+
+def test_overlap_schedule_order(monkeypatch):
+    """The overlapped launch order (SlabSolver.overlap): edge rows, exchange
+    posted on the comm context, inner rows, wait + fence -- recorded on a stub
+    backend (no process group needed)."""
+    import contextlib
+
+    log = []
+
+    class Stub:
+        def reserve(self, n):
+            self.n = n
+
+        def run(self, src, dst, weights, first, nsteps, off, rows=None):
+            log.append(("run", rows))
+
+        def layers(self, buf, first, count):
+            return torch.zeros(1)
+
+        def norms(self, n):
+            return torch.zeros(2 * n, dtype=torch.float64)
+
+        @contextlib.contextmanager
+        def comm(self):
+            log.append(("comm",))
+            yield
+
+        def comm_fence(self):
+            log.append(("fence",))
+
+    class Req:
+        def wait(self):
+            log.append(("wait",))
+
+    d = SlabDecomposition(40, 3, 1, halo=3)
+    solver = SlabSolver(Stub(), d, fuse=3)
+    assert solver.overlap
+    monkeypatch.setattr(solver, "_post_exchange", lambda buf: log.append(("post",)) or [Req()])
+    monkeypatch.setattr(dist, "all_reduce", lambda *a, **k: None)
+    solver.run(0, np.array([1.0]), 0, 3)
+    assert log == [("run", (3, 6)), ("run", (13, 16)), ("comm",), ("post",), ("run", (6, 13)),
+                   ("comm",), ("wait",), ("fence",)]
+    monkeypatch.setenv("SRJ_SLAB_OVERLAP", "0")
+    assert not SlabSolver(Stub(), d, fuse=3).overlap
