@@ -188,3 +188,28 @@ def test_fused_faces_degenerate_2d(shape):
 def test_fused_faces_degenerate_3d(shape):
     bc = (((M, None), (F, 0.5)), ((F, -1.5), (M, None)), ((M, None), (F, 2.0)))
     _run(shape, bc, 2, 7, seed=sum(shape))
+
+
+@pytest.mark.parametrize("shape,fuse", [((24, 30, 70), 2), ((600, 520), 4)])
+def test_fused_faces_nonlinear_source(shape, fuse):
+    """Fused faces with the nonlinear source s = kappa * psi^5 (cfg5 form)."""
+    from paper_1511_04292_b200.problems import nonlinear_fields
+
+    f = nonlinear_fields(shape, seed=3)
+    nd = len(shape)
+    bc = (((M, None), (F, 1.0)),) + (((M, None), (M, None)),) * (nd - 1)
+    rules = tuple(tuple(_rule(k, v) for k, v in pair) for pair in bc)
+    w = np.array([1.4, 0.7, 0.9, 0.6])
+
+    def make(rules):
+        return G.GridProblem(spacing=(1.0,) * nd, u=np.array(f["u"], dtype=float),
+                             source=np.zeros(shape), center=f["center"], lower=f["lower"],
+                             upper=f["upper"], bc=rules, source_kappa=f["kappa"])
+
+    p = make(rules)
+    q = make(((G.FIXED, G.FIXED),) * nd)
+    q.u[...] = p.u
+    hist, _ = G.srj_solve(p, Cycle(w), 1e-300, max_iters=14, fuse=fuse)
+    _, _, norms = oracle.run_bc(q, bc, w, 14, kappa=f["kappa"])
+    assert np.array_equal(p.u, q.u)
+    assert np.array_equal(hist.true_residual_inf, norms[:, 1])
