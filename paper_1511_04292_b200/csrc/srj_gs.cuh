@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams 
     double c[1 + 2 * ND];
     bool act;
   };
-  constexpr int kPF = 4;
+  // ring depth: deeper rings hide more of the per-step latency (4096^2:
+  // kPF 4 / 6 / 9 / 14 -> 9.9 / 10.8 / 11.8 / 12.4 GLUPS) within 255
+  // registers (2D constant 240-250; the 3D and per-cell rings hold more)
+  constexpr int kPF = VAR ? 4 : (ND == 2 ? 14 : 6);
 
 #pragma unroll 1
   for (int k = 0; k < p.nsweeps; ++k) {
