@@ -9,7 +9,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
+#include <mutex>
+#include <vector>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -17,42 +20,19 @@
 #include <cstring>
 
 #include "../../include/srj.h"
+#include "srj_host.cuh"
 #include "srj_reduce.cuh"
-#include "srj_sweep2d.cuh"
-#include "srj_sweep3d.cuh"
 #include "srj_cluster2d.cuh"
-#include "srj_gs.cuh"
 #include "srj_sweep2d_var.cuh"
-#include "srj_sweep3d_tb.cuh"
 
 using namespace srj;
+using namespace srj_host;
 
 namespace {
 
 constexpr int64_t kAlign = 16;        // elements (128 B)
 constexpr int64_t kXOff = kAlign - 1; // last-axis ghost g=0 sits at offset 15
 constexpr int64_t kSlack = 256;       // tail elements for band over-reads
-
-thread_local char g_err[512] = "";
-
-int fail(int code, const char *fmt, ...) {
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(g_err, sizeof(g_err), fmt, ap);
-  va_end(ap);
-  return code;
-}
-
-int cuda_fail(cudaError_t e, const char *what) {
-  return fail(e == cudaErrorMemoryAllocation ? SRJ_ENOMEM : SRJ_ECUDA, "%s: %s", what,
-              cudaGetErrorString(e));
-}
-
-#define SRJ_CUDA(call)                                  \
-  do {                                                  \
-    cudaError_t e_ = (call);                            \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
-  } while (0)
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
@@ -96,132 +76,6 @@ int bps_override() {
   return b;
 }
 
-// Per-device caches: function attributes and occupancy belong to a device
-// context, so one process may drive several GPUs (from several threads).
-// Races only repeat idempotent work.
-constexpr int kMaxDevices = 64;
-
-int current_device() {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  return dev & (kMaxDevices - 1);
-}
-
-// Runs f() once per device for the given cache of flags.
-template <typename F>
-void once_per_device(std::atomic<uint64_t> &done, F &&f) {
-  const uint64_t bit = uint64_t(1) << current_device();
-  if (done.load(std::memory_order_acquire) & bit) return;
-  f();
-  done.fetch_or(bit, std::memory_order_acq_rel);
-}
-
-// Per-device integer cache filled by f() (0 = not yet computed).
-template <typename F>
-int cached_per_device(std::atomic<int> (&slot)[kMaxDevices], F &&f) {
-  std::atomic<int> &v = slot[current_device()];
-  int n = v.load(std::memory_order_acquire);
-  if (n == 0) {
-    n = f();
-    v.store(n, std::memory_order_release);
-  }
-  return n;
-}
-
-int sm_count() {
-  static std::atomic<int> cache[kMaxDevices];
-  return cached_per_device(cache, [] {
-    int n = 0;
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device());
-    return n > 0 ? n : 148;
-  });
-}
-
-// ------------------------------------------------------------ 2D dispatch
-constexpr int kMaxFuseBC = 4;  // 2D fused depth with MIRROR / FACE_DIRICHLET faces
-
-// One entry per kernel instantiation: launcher + resident blocks per SM
-// (registers and shared memory both counted, from the occupancy API), so the
-// launch can be sized to exactly one wave.
-struct Kernel2D {
-  void (*launch)(const Sweep2DParams &, const CUtensorMap &, const CUtensorMap &, int blocks,
-                 cudaStream_t);
-  int box_cols;
-  int (*blocks_per_sm)();
-  int own;  // columns owned per band
-};
-
-template <int T, bool VAR, bool NL, bool RECIP, int BCF = 0>
-struct K2 {
-  static constexpr int V = 2;
-  using B = Band2D<T, V>;
-  static void configure() {
-    static std::atomic<uint64_t> done{0};
-    once_per_device(done, [] {
-      cudaFuncSetAttribute(sweep2d_tb<T, V, VAR, NL, RECIP, BCF>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(B::smem_bytes()));
-    });
-  }
-  static void launch(const Sweep2DParams &p, const CUtensorMap &tu, const CUtensorMap &tf,
-                     int blocks, cudaStream_t s) {
-    configure();
-    sweep2d_tb<T, V, VAR, NL, RECIP, BCF><<<blocks, B::WARPS * 32, B::smem_bytes(), s>>>(p, tu, tf);
-  }
-  static int bps() {
-    static std::atomic<int> cache[kMaxDevices];
-    return cached_per_device(cache, [] {
-      configure();
-      int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_tb<T, V, VAR, NL, RECIP, BCF>,
-                                                    B::WARPS * 32, B::smem_bytes());
-      return n > 0 ? n : 1;
-    });
-  }
-  static Kernel2D get() { return Kernel2D{launch, B::BAND, bps, B::OWN}; }
-};
-
-template <int T, int BCF>
-Kernel2D pick2d_bc(bool var, bool nl, bool recip) {
-  if (var) return nl ? K2<T, true, true, false, BCF>::get() : K2<T, true, false, false, BCF>::get();
-  if (recip) return nl ? K2<T, false, true, true, BCF>::get() : K2<T, false, false, true, BCF>::get();
-  return nl ? K2<T, false, true, false, BCF>::get() : K2<T, false, false, false, BCF>::get();
-}
-
-// bcf: 0 = FIXED faces; 1 = fused MIRROR / FACE_DIRICHLET faces; 2 = the same
-// with MIRROR-or-FIXED column faces (no face values in the edge-band path)
-template <int T>
-Kernel2D pick2d_t(bool var, bool nl, bool recip, int bcf) {
-  if constexpr (T >= 2 && T <= kMaxFuseBC) {
-    if (bcf == 1) return pick2d_bc<T, 1>(var, nl, recip);
-    if (bcf == 2) return pick2d_bc<T, 2>(var, nl, recip);
-  }
-  if (var) return nl ? K2<T, true, true, false>::get() : K2<T, true, false, false>::get();
-  if (recip) return nl ? K2<T, false, true, true>::get() : K2<T, false, false, true>::get();
-  return nl ? K2<T, false, true, false>::get() : K2<T, false, false, false>::get();
-}
-
-// ------------------------------------------------------------ 3D dispatch
-struct Kernel3D {
-  void (*launch)(const Sweep3DParams &, int blocks, cudaStream_t);
-  int (*blocks_per_sm)();
-};
-
-template <bool VAR, bool NL, bool RECIP>
-struct K3 {
-  static void launch(const Sweep3DParams &p, int blocks, cudaStream_t s) {
-    sweep3d<VAR, NL, RECIP><<<blocks, kWarps3D * 32, 0, s>>>(p);
-  }
-  static int bps() {
-    static std::atomic<int> cache[kMaxDevices];
-    return cached_per_device(cache, [] {
-      int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d<VAR, NL, RECIP>, kWarps3D * 32, 0);
-      return n > 0 ? n : 1;
-    });
-  }
-  static Kernel3D get() { return Kernel3D{launch, bps}; }
-};
-
 // 2D per-cell coefficients, one sweep (HBM-bound streaming kernel)
 template <bool NL>
 struct KVar2D {
@@ -235,8 +89,9 @@ struct KVar2D {
   }
 };
 
-static int launch_var2d(const srj_plan_desc &d, const double *cur, double *nxt, const double *f,
-                        int ld_lo, int ld_hi, double omega, double *norms, cudaStream_t st) {
+static int launch_var2d(const srj_plan_desc &d, int64_t own_b, int64_t own_e, const double *cur,
+                        double *nxt, const double *f, int ld_lo, int ld_hi, double omega,
+                        double *norms, cudaStream_t st) {
   const srj_layout_t &l = d.layout;
   const int64_t ioff = interior_offset(l);
   const bool nl = d.kappa != nullptr;
@@ -255,8 +110,8 @@ static int launch_var2d(const srj_plan_desc &d, const double *cur, double *nxt, 
   p.n1 = int(l.n[1]);
   p.ld_lo = ld_lo;
   p.ld_hi = ld_hi;
-  p.own_b = int(d.own0_begin);
-  p.own_e = int(d.own0_end);
+  p.own_b = int(own_b);
+  p.own_e = int(own_e);
   p.nbands = int((l.n[1] + 63) / 64);
   p.omega = omega;
   p.norms = norms;
@@ -288,104 +143,6 @@ static int launch_var2d(const srj_plan_desc &d, const double *cur, double *nxt, 
   return SRJ_OK;
 }
 
-// Gauss-Seidel / SOR wavefront (srj_gs.cuh): nsweeps in-place sweeps, one
-// cooperative launch (every strip co-resident)
-template <int ND, bool VAR, bool RECIP>
-static int launch_gs_t(const GSParams &p, int nstrips, cudaStream_t st) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(nstrips);
-  cfg.blockDim = dim3(32);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, gs_sweep<ND, VAR, RECIP>, p);
-  if (e == cudaErrorCooperativeLaunchTooLarge)
-    return fail(SRJ_EUNSUPPORTED, "Gauss-Seidel wavefront needs %d co-resident strips of 32 rows; "
-                "the grid has too many rows for one GPU", nstrips);
-  SRJ_CUDA(e);
-  return SRJ_OK;
-}
-
-static int launch_gs(const GSParams &p, int nd, bool var, bool recip, int nstrips, cudaStream_t st) {
-  if (nd == 2) {
-    if (var) return launch_gs_t<2, true, false>(p, nstrips, st);
-    return recip ? launch_gs_t<2, false, true>(p, nstrips, st)
-                 : launch_gs_t<2, false, false>(p, nstrips, st);
-  }
-  if (var) return launch_gs_t<3, true, false>(p, nstrips, st);
-  return recip ? launch_gs_t<3, false, true>(p, nstrips, st)
-               : launch_gs_t<3, false, false>(p, nstrips, st);
-}
-
-// temporally blocked 3D (constant stencil only)
-constexpr int kMaxFuse3D = 3;  // T=4 tiles exceed shared memory
-
-struct Kernel3DTB {
-  void (*launch)(const Sweep3DTBParams &, const CUtensorMap &, const CUtensorMap &, int,
-                 cudaStream_t);
-  int (*blocks_per_sm)();
-  int tj, tk, box_cols, box_rows;
-};
-
-template <int T, bool NL, bool RECIP, int BCF = 0>
-struct K3TB {
-  using B = Tile3D<T>;
-  static void configure() {
-    static std::atomic<uint64_t> done{0};
-    once_per_device(done, [] {
-      cudaFuncSetAttribute(sweep3d_tb<T, NL, RECIP, BCF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(B::smem_bytes()));
-    });
-  }
-  static void launch(const Sweep3DTBParams &p, const CUtensorMap &tu, const CUtensorMap &tf,
-                     int blocks, cudaStream_t s) {
-    configure();
-    sweep3d_tb<T, NL, RECIP, BCF><<<blocks, B::THREADS, B::smem_bytes(), s>>>(p, tu, tf);
-  }
-  static int bps() {
-    static std::atomic<int> cache[kMaxDevices];
-    return cached_per_device(cache, [] {
-      configure();
-      int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d_tb<T, NL, RECIP, BCF>, B::THREADS,
-                                                    B::smem_bytes());
-      return n > 0 ? n : 1;
-    });
-  }
-  static Kernel3DTB get() { return Kernel3DTB{launch, bps, B::TJ, B::TK, B::HS, B::HJ}; }
-};
-
-template <int T, int BCF>
-Kernel3DTB pick3d_tb_bc(bool nl, bool recip) {
-  if (recip) return nl ? K3TB<T, true, true, BCF>::get() : K3TB<T, false, true, BCF>::get();
-  return nl ? K3TB<T, true, false, BCF>::get() : K3TB<T, false, false, BCF>::get();
-}
-
-// bcf: 0 = FIXED faces; 1 = fused MIRROR / FACE_DIRICHLET faces; 2 = MIRROR only
-template <int T>
-Kernel3DTB pick3d_tb_t(bool nl, bool recip, int bcf) {
-  if (bcf == 1) return pick3d_tb_bc<T, 1>(nl, recip);
-  if (bcf == 2) return pick3d_tb_bc<T, 2>(nl, recip);
-  if (recip) return nl ? K3TB<T, true, true>::get() : K3TB<T, false, true>::get();
-  return nl ? K3TB<T, true, false>::get() : K3TB<T, false, false>::get();
-}
-
-Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf) {
-  switch (T) {
-    case 2: return pick3d_tb_t<2>(nl, recip, bcf);
-    default: return pick3d_tb_t<3>(nl, recip, bcf);
-  }
-}
-
-Kernel3D pick3d(bool var, bool nl, bool recip) {
-  if (var) return nl ? K3<true, true, false>::get() : K3<true, false, false>::get();
-  if (recip) return nl ? K3<false, true, true>::get() : K3<false, false, true>::get();
-  return nl ? K3<false, true, false>::get() : K3<false, false, false>::get();
-}
-
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -398,6 +155,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
   }
   return fn;
+}
+
+Kernel2D pick2d(int T, bool var, bool nl, bool recip, int bcf) {
+  switch (T) {
+    case 1: return pick2d_t<1>(var, nl, recip, bcf);
+    case 2: return pick2d_t<2>(var, nl, recip, bcf);
+    case 3: return pick2d_t<3>(var, nl, recip, bcf);
+    case 4: return pick2d_t<4>(var, nl, recip, bcf);
+    case 5: return pick2d_t<5>(var, nl, recip, bcf);
+    case 6: return pick2d_t<6>(var, nl, recip, bcf);
+    case 7: return pick2d_t<7>(var, nl, recip, bcf);
+    default: return pick2d_t<8>(var, nl, recip, bcf);
+  }
 }
 
 // 2D tensor map over a whole padded 2D field: rows0 rows of `pitch` doubles,
@@ -417,19 +187,6 @@ int make_tmap(CUtensorMap *m, const double *base, const srj_layout_t &l, int box
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SRJ_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return SRJ_OK;
-}
-
-Kernel2D pick2d(int T, bool var, bool nl, bool recip, int bcf) {
-  switch (T) {
-    case 1: return pick2d_t<1>(var, nl, recip, bcf);
-    case 2: return pick2d_t<2>(var, nl, recip, bcf);
-    case 3: return pick2d_t<3>(var, nl, recip, bcf);
-    case 4: return pick2d_t<4>(var, nl, recip, bcf);
-    case 5: return pick2d_t<5>(var, nl, recip, bcf);
-    case 6: return pick2d_t<6>(var, nl, recip, bcf);
-    case 7: return pick2d_t<7>(var, nl, recip, bcf);
-    default: return pick2d_t<8>(var, nl, recip, bcf);
-  }
 }
 
 }  // namespace
@@ -466,7 +223,37 @@ struct srj_plan {
   int64_t *g_dst = nullptr, *g_src = nullptr;
   double *g_tmp = nullptr;
   int64_t g_n = 0;
+  // encoded TMA descriptors by (base, box): a solve cycles through 3 field
+  // buffers and one source array, so a handful of entries avoids re-encoding
+  // two descriptors per launch on the host
+  struct Tmap {
+    CUtensorMap m;
+    const void *base = nullptr;
+    int cols = 0, rows = 0;
+  };
+  Tmap tmaps[8];
+  int tmap_next = 0;
 };
+
+static int plan_tmap(srj_plan &plan, CUtensorMap *out, const double *base, int box_cols, int box_rows) {
+  for (const auto &t : plan.tmaps)
+    if (t.base == base && t.cols == box_cols && t.rows == box_rows) {
+      *out = t.m;
+      return SRJ_OK;
+    }
+  srj_plan::Tmap &t = plan.tmaps[plan.tmap_next];
+  plan.tmap_next = (plan.tmap_next + 1) % 8;
+  const int rc = make_tmap(&t.m, base, plan.d.layout, box_cols, box_rows);
+  if (rc != SRJ_OK) {
+    t.base = nullptr;
+    return rc;
+  }
+  t.base = base;
+  t.cols = box_cols;
+  t.rows = box_rows;
+  *out = t.m;
+  return SRJ_OK;
+}
 
 static void free_gather(srj_plan *p) {
   if (p->g_dst) cudaFree(p->g_dst);
@@ -742,6 +529,65 @@ int small_mode() {
   return v;
 }
 
+template <bool VAR, bool NL, bool RECIP>
+static void configure_cluster() {
+  static std::atomic<uint64_t> configured{0};
+  once_per_device(configured, [] {
+    cudaFuncSetAttribute(sweep2d_cluster<VAR, NL, RECIP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(sweep2d_cluster<VAR, NL, RECIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+  });
+}
+
+static cudaLaunchConfig_t cluster_config(int C, size_t smem, cudaStream_t st, cudaLaunchAttribute *attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(kClusterThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+// Can a C-CTA cluster with `smem` bytes per CTA be co-scheduled on this
+// device at all (a MIG slice or a partly busy GPC may not hold 16 CTAs)?
+// Cached per (device, C, smem); a "no" sends the plan to the band kernel.
+template <bool VAR, bool NL, bool RECIP>
+static bool cluster_schedulable_t(int C, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::array<int64_t, 4>> cache;  // device, C, smem, ok
+  const int dev = current_device();
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto &e : cache)
+      if (e[0] == dev && e[1] == C && e[2] == int64_t(smem)) return e[3] != 0;
+  }
+  configure_cluster<VAR, NL, RECIP>();
+  cudaLaunchAttribute attr[1];
+  const cudaLaunchConfig_t cfg = cluster_config(C, smem, nullptr, attr);
+  int n = 0;
+  const bool ok = cudaOccupancyMaxActiveClusters(&n, sweep2d_cluster<VAR, NL, RECIP>, &cfg) == cudaSuccess && n >= 1;
+  cudaGetLastError();
+  std::lock_guard<std::mutex> lk(mu);
+  cache.push_back({dev, C, int64_t(smem), ok ? 1 : 0});
+  return ok;
+}
+
+static bool cluster_schedulable(const srj_plan &plan, int C, int R) {
+  const srj_plan_desc &d = plan.d;
+  const bool var = d.coef_mode == 1, nl = d.kappa != nullptr;
+  const bool recip = !var && recip_or_zero(d.coef[0]) != 0.0;
+  const size_t smem = 2 * size_t(R + 2) * size_t(d.layout.n[1] + 2) * 8;
+  if (var) return nl ? cluster_schedulable_t<true, true, false>(C, smem) : cluster_schedulable_t<true, false, false>(C, smem);
+  if (recip) return nl ? cluster_schedulable_t<false, true, true>(C, smem) : cluster_schedulable_t<false, false, true>(C, smem);
+  return nl ? cluster_schedulable_t<false, true, false>(C, smem) : cluster_schedulable_t<false, false, false>(C, smem);
+}
+
 static bool cluster_fits(const srj_plan &plan, int &C, int &R) {
   const srj_plan_desc &d = plan.d;
   const srj_layout_t &l = d.layout;
@@ -756,29 +602,14 @@ static bool cluster_fits(const srj_plan &plan, int &C, int &R) {
   C = (n0 + R - 1) / R;
   if (R > kTY * kMaxA || l.n[1] > kTX * kMaxB) return false;  // register tiling limits
   const size_t bytes = 2 * size_t(R + 2) * size_t(l.n[1] + 2) * 8;
-  return bytes <= 200 * 1024;
+  return bytes <= 200 * 1024 && cluster_schedulable(plan, C, R);
 }
 
 template <bool VAR, bool NL, bool RECIP>
 static int launch_cluster(const Cluster2DParams &p, int C, size_t smem, cudaStream_t st) {
-  static std::atomic<uint64_t> configured{0};
-  once_per_device(configured, [] {
-    cudaFuncSetAttribute(sweep2d_cluster<VAR, NL, RECIP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(sweep2d_cluster<VAR, NL, RECIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-  });
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C, 1, 1);
-  cfg.blockDim = dim3(kClusterThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
+  configure_cluster<VAR, NL, RECIP>();
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  const cudaLaunchConfig_t cfg = cluster_config(C, smem, st, attr);
   SRJ_CUDA(cudaLaunchKernelEx(&cfg, sweep2d_cluster<VAR, NL, RECIP>, p));
   return SRJ_OK;
 }
@@ -856,6 +687,216 @@ static int run_cluster2d(srj_plan &plan, const double *src, double *dst, const d
   return SRJ_OK;
 }
 
+// One launch of t fused sweeps (weights om[0..t)) from `cur` into `nxt`,
+// relaxing, storing and counting local axis-0 rows [own_b, own_e) only (the
+// plan's own range, or a part of it: the slab exchange's edge / inner
+// launches).  Per-step (dmax, rmax) are folded into norms[2*q..] with
+// atomicMax, so several parts of one step may share a norm slot.
+static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const double *cur,
+                        double *nxt, const double *om, int t, double *norms, cudaStream_t st) {
+  const srj_plan_desc &d = plan.d;
+  const srj_layout_t &l = d.layout;
+  const int64_t ioff = interior_offset(l);
+  const bool var = d.coef_mode == 1;
+  const bool nl = d.kappa != nullptr;
+  const double *f = nl ? d.kappa : d.source;
+  int lo_c, hi_c, ld_lo, ld_hi;
+  row_ranges(d, lo_c, hi_c, ld_lo, ld_hi);
+  const int rows = int(own_e - own_b);
+  if (l.ndim == 2 && var && t == 1) {
+    const int rc = launch_var2d(d, own_b, own_e, cur, nxt, f, ld_lo, ld_hi, om[0], norms, st);
+    if (rc != SRJ_OK) return rc;
+  } else if (l.ndim == 2) {
+    Sweep2DParams p{};
+    p.src = cur + ioff;
+    p.dst = nxt + ioff;
+    p.f = f + ioff;
+    p.act = d.act ? d.act + ioff : nullptr;
+    if (var) {
+      p.c = d.coef_arrays[0] + ioff;
+      p.am0 = d.coef_arrays[1] + ioff;
+      p.ap0 = d.coef_arrays[2] + ioff;
+      p.am1 = d.coef_arrays[3] + ioff;
+      p.ap1 = d.coef_arrays[4] + ioff;
+    }
+    p.kc = d.coef[0];
+    p.kam0 = d.coef[1];
+    p.kap0 = d.coef[2];
+    p.kam1 = d.coef[3];
+    p.kap1 = d.coef[4];
+    p.kinv = recip_or_zero(d.coef[0]);
+    p.kinv_lo = recip_lo(d.coef[0], p.kinv);
+    p.pitch = l.pitch;
+    p.n0 = int(l.n[0]);
+    p.n1 = int(l.n[1]);
+    p.lo_c = lo_c;
+    p.hi_c = hi_c;
+    p.ld_lo = ld_lo;
+    p.ld_hi = ld_hi;
+    p.own_b = int(own_b);
+    p.own_e = int(own_e);
+    int bcf = 0;
+    if (plan.has_bc && t > 1) {
+      bcf = 2;
+      for (int side = 0; side < 2; ++side)
+        if (d.bc[1][side].kind == SRJ_BC_FACE_DIRICHLET) bcf = 1;
+    }
+    const Kernel2D k2 = pick2d(t, var, nl, !var && p.kinv != 0.0, bcf);
+    p.nbands = int((l.n[1] + k2.own - 1) / k2.own);
+    // strips x bands = waves x resident warps (default one wave)
+    const int bps = bps_override() > 0 ? std::min(bps_override(), k2.blocks_per_sm())
+                                       : k2.blocks_per_sm();
+    const int capacity = sm_count() * bps * Band2D<1, 2>::WARPS * waves_2d();
+    int nstrips = std::max(1, capacity / p.nbands);
+    nstrips = std::min(nstrips, std::max(1, rows / std::max(2 * t, 8)));
+    p.H = (rows + nstrips - 1) / nstrips;
+    p.nstrips = (rows + p.H - 1) / p.H;
+    for (int q = 0; q < t; ++q) p.omega[q] = om[q];
+    p.norms = norms;
+    p.tma_col0 = int(l.origin + 1);
+    p.tma_row0 = l.halo0;
+    for (int a = 0; a < 2; ++a)
+      for (int side = 0; side < 2; ++side) {
+        const srj_face_rule &b = d.bc[a][side];
+        p.bc_kind[a][side] = b.kind;
+        const bool arr = b.kind == SRJ_BC_FACE_DIRICHLET && b.values;
+        p.bc_ptr[a][side] = arr ? b.values : plan.bc_scalars + 2 * a + side;
+        p.bc_step[a][side] = arr ? 1 : 0;
+      }
+    CUtensorMap tu, tf;
+    int rc = plan_tmap(plan, &tu, cur, k2.box_cols, 3);
+    if (rc != SRJ_OK) return rc;
+    rc = plan_tmap(plan, &tf, f, k2.box_cols, 3);
+    if (rc != SRJ_OK) return rc;
+    const int warps = p.nbands * p.nstrips;
+    const int blocks = (warps + Band2D<1, 2>::WARPS - 1) / Band2D<1, 2>::WARPS;
+    k2.launch(p, tu, tf, blocks, st);
+  } else if (t > 1) {
+    // temporally blocked 3D (constant stencil): t fused sweeps per launch
+    Sweep3DTBParams p{};
+    p.dst = nxt + ioff;
+    for (int a = 0; a < 7; ++a) p.kc[a] = d.coef[a];
+    p.kinv = recip_or_zero(d.coef[0]);
+    p.kinv_lo = recip_lo(d.coef[0], p.kinv);
+    p.pitch = l.pitch;
+    p.plane = l.plane;
+    p.n0 = int(l.n[0]);
+    p.n1 = int(l.n[1]);
+    p.n2 = int(l.n[2]);
+    p.ld_lo = ld_lo;
+    p.ld_hi = ld_hi;
+    p.own_b = int(own_b);
+    p.own_e = int(own_e);
+    p.tma_col0 = int(l.origin + 1);
+    p.rows_per_plane = int(l.n[1] + 2);
+    p.tma_row0 = l.halo0 * p.rows_per_plane + 1;  // row of (i=0, j=0)
+    for (int q = 0; q < t; ++q) p.omega[q] = om[q];
+    p.norms = norms;
+    for (int a = 0; a < 3; ++a)
+      for (int side = 0; side < 2; ++side) {
+        const srj_face_rule &b = d.bc[a][side];
+        p.bc_kind[a][side] = b.kind;
+        const bool arr = b.kind == SRJ_BC_FACE_DIRICHLET && b.values;
+        p.bc_ptr[a][side] = arr ? b.values : plan.bc_scalars + 2 * a + side;
+        p.bc_step[a][side] = arr ? 1 : 0;
+      }
+    int bcf = 0;
+    if (plan.has_bc) {
+      bcf = 2;
+      for (int a = 0; a < 3; ++a)
+        for (int side = 0; side < 2; ++side)
+          if (d.bc[a][side].kind == SRJ_BC_FACE_DIRICHLET) bcf = 1;
+    }
+    const Kernel3DTB k3 = pick3d_tb(t, nl, p.kinv != 0.0, bcf);
+    p.ntj = int((l.n[1] + k3.tj - 1) / k3.tj);
+    p.ntk = int((l.n[2] + k3.tk - 1) / k3.tk);
+    const long tiles = long(p.ntj) * p.ntk;
+    const long capacity = long(sm_count()) * k3.blocks_per_sm();
+    int nstrips = 1;
+    double best = -1.0;
+    for (int ns = 1; ns <= std::max(1, std::min(64, rows / (4 * t))); ++ns) {
+      const long w = tiles * ns;
+      const long waves = (w + capacity - 1) / capacity;
+      const double hh = double(rows) / ns;
+      const double eff = double(w) / double(waves * capacity) * hh / (hh + 2.0 * t);
+      if (eff > best + 1e-9) {
+        best = eff;
+        nstrips = ns;
+      }
+    }
+    p.H = (rows + nstrips - 1) / nstrips;
+    p.nstrips = (rows + p.H - 1) / p.H;
+    CUtensorMap tu, tf;
+    int rc = plan_tmap(plan, &tu, cur, k3.box_cols, k3.box_rows);
+    if (rc != SRJ_OK) return rc;
+    rc = plan_tmap(plan, &tf, f, k3.box_cols, k3.box_rows);
+    if (rc != SRJ_OK) return rc;
+    k3.launch(p, tu, tf, int(tiles * p.nstrips), st);
+  } else {
+    Sweep3DParams p{};
+    p.src = cur + ioff;
+    p.dst = nxt + ioff;
+    p.f = f + ioff;
+    p.act = d.act ? d.act + ioff : nullptr;
+    for (int a = 0; a < 7; ++a) {
+      p.coef[a] = var ? d.coef_arrays[a] + ioff : nullptr;
+      p.kc[a] = d.coef[a];
+    }
+    p.pitch = l.pitch;
+    p.plane = l.plane;
+    p.n0 = int(l.n[0]);
+    p.n1 = int(l.n[1]);
+    p.n2 = int(l.n[2]);
+    // one-deep stencil: only owned rows relax; exchanged halos are inputs
+    p.lo_c = 0;
+    p.hi_c = p.n0;
+    p.ld_lo = ld_lo;
+    p.ld_hi = ld_hi;
+    p.own_b = int(own_b);
+    p.own_e = int(own_e);
+    p.nbands = int((l.n[2] + 63) / 64);
+    p.njg = int((l.n[1] + kRows3D - 1) / kRows3D);
+    p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
+    p.kinv_lo = recip_lo(d.coef[0], p.kinv);
+    const bool recip = !var && p.kinv != 0.0;
+    const Kernel3D k3 = pick3d(var, nl, recip);
+    const long per_strip = long(p.njg) * p.nbands;
+    const long capacity = long(sm_count()) * k3.blocks_per_sm() * kWarps3D;
+    // strips: best fill of whole waves, discounting the 2 halo planes per strip
+    int nstrips = 1;
+    double best = -1.0;
+    for (int ns = 1; ns <= std::max(1, std::min(64, rows / 8)); ++ns) {
+      const long w = per_strip * ns;
+      const long waves = (w + capacity - 1) / capacity;
+      const double hh = double(rows) / ns;
+      const double eff = double(w) / double(waves * capacity) * hh / (hh + 2.0);
+      if (eff > best + 1e-9) {
+        best = eff;
+        nstrips = ns;
+      }
+    }
+    p.H = (rows + nstrips - 1) / nstrips;
+    p.nstrips = (rows + p.H - 1) / p.H;
+    p.omega = om[0];
+    p.norms = norms;
+    const long warps = per_strip * p.nstrips;
+    k3.launch(p, int((warps + kWarps3D - 1) / kWarps3D), st);
+  }
+  SRJ_CUDA(cudaGetLastError());
+  return SRJ_OK;
+}
+
+// effective fused depth for a plan (srj_plan_run's rules)
+static int plan_depth(const srj_plan &plan, int fuse) {
+  const srj_plan_desc &d = plan.d;
+  const srj_layout_t &l = d.layout;
+  int T = fuse > 0 ? fuse : plan.default_fuse;
+  if ((plan.has_bc && !plan.bc_fusable) || plan.g_n > 0 || (l.ndim == 3 && d.coef_mode == 1)) T = 1;
+  if (plan.has_bc && T > kMaxFuseBC) T = kMaxFuseBC;
+  if (l.ndim == 3 && T > kMaxFuse3D) T = kMaxFuse3D;
+  return T;
+}
+
 extern "C" {
 
 int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b,
@@ -873,24 +914,13 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
   const srj_plan_desc &d = plan->d;
   const srj_layout_t &l = d.layout;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int T = fuse > 0 ? fuse : plan->default_fuse;
-  if ((plan->has_bc && !plan->bc_fusable) || plan->g_n > 0 || (l.ndim == 3 && d.coef_mode == 1))
-    T = 1;
-  if (plan->has_bc && T > kMaxFuseBC) T = kMaxFuseBC;
-  if (l.ndim == 3 && T > kMaxFuse3D) T = kMaxFuse3D;
+  const int T = plan_depth(*plan, fuse);
   if (T > kMaxFuse) return fail(SRJ_EINVAL, "fuse depth %d exceeds %d", T, kMaxFuse);
-  if ((!d.physical_lo0 || !d.physical_hi0) && T > l.halo0)
+  if ((!d.physical_lo0 || !d.physical_hi0) && T > l.halo0 && T > 1)
     return fail(SRJ_EINVAL, "fuse depth %d needs halo0 >= %d on exchanged faces", T, T);
 
   SRJ_CUDA(cudaMemsetAsync(d_norms, 0, sizeof(double) * 2 * size_t(nsteps), st));
   const int64_t ioff = interior_offset(l);
-  const bool var = d.coef_mode == 1;
-  const bool nl = d.kappa != nullptr;
-  const double *f = nl ? d.kappa : d.source;
-  int lo_c, hi_c, ld_lo, ld_hi;
-  row_ranges(d, lo_c, hi_c, ld_lo, ld_hi);
-  const int rows = int(d.own0_end - d.own0_begin);
-
   if (l.ndim == 2 && plan->g_n == 0) {
     int C = 0, R = 0;
     if (cluster_fits(*plan, C, R)) return run_cluster2d(*plan, src, buf_a, weights, m, first, nsteps, d_norms, final_buf, st, C, R);
@@ -901,193 +931,16 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
   int64_t k = 0;
   while (k < nsteps) {
     const int t = int(std::min<int64_t>(T, nsteps - k));
-    if (l.ndim == 2 && var && t == 1) {
-      const int rc = launch_var2d(d, cur, nxt, f, ld_lo, ld_hi, weights[(first + k) % m],
-                                  d_norms + 2 * k, st);
-      if (rc != SRJ_OK) return rc;
-    } else if (l.ndim == 2) {
-      Sweep2DParams p{};
-      p.src = cur + ioff;
-      p.dst = nxt + ioff;
-      p.f = f + ioff;
-      p.act = d.act ? d.act + ioff : nullptr;
-      if (var) {
-        p.c = d.coef_arrays[0] + ioff;
-        p.am0 = d.coef_arrays[1] + ioff;
-        p.ap0 = d.coef_arrays[2] + ioff;
-        p.am1 = d.coef_arrays[3] + ioff;
-        p.ap1 = d.coef_arrays[4] + ioff;
-      }
-      p.kc = d.coef[0];
-      p.kam0 = d.coef[1];
-      p.kap0 = d.coef[2];
-      p.kam1 = d.coef[3];
-      p.kap1 = d.coef[4];
-      p.kinv = recip_or_zero(d.coef[0]);
-      p.kinv_lo = recip_lo(d.coef[0], p.kinv);
-      p.pitch = l.pitch;
-      p.n0 = int(l.n[0]);
-      p.n1 = int(l.n[1]);
-      p.lo_c = lo_c;
-      p.hi_c = hi_c;
-      p.ld_lo = ld_lo;
-      p.ld_hi = ld_hi;
-      p.own_b = int(d.own0_begin);
-      p.own_e = int(d.own0_end);
-      int bcf = 0;
-      if (plan->has_bc && t > 1) {
-        bcf = 2;
-        for (int side = 0; side < 2; ++side)
-          if (d.bc[1][side].kind == SRJ_BC_FACE_DIRICHLET) bcf = 1;
-      }
-      const Kernel2D k2 = pick2d(t, var, nl, !var && p.kinv != 0.0, bcf);
-      p.nbands = int((l.n[1] + k2.own - 1) / k2.own);
-      // strips x bands = waves x resident warps (default one wave)
-      const int bps = bps_override() > 0 ? std::min(bps_override(), k2.blocks_per_sm())
-                                         : k2.blocks_per_sm();
-      const int capacity = sm_count() * bps * Band2D<1, 2>::WARPS * waves_2d();
-      int nstrips = std::max(1, capacity / p.nbands);
-      nstrips = std::min(nstrips, std::max(1, rows / std::max(2 * t, 8)));
-      p.H = (rows + nstrips - 1) / nstrips;
-      p.nstrips = (rows + p.H - 1) / p.H;
-      for (int q = 0; q < t; ++q) p.omega[q] = weights[(first + k + q) % m];
-      p.norms = d_norms + 2 * k;
-      p.tma_col0 = int(l.origin + 1);
-      p.tma_row0 = l.halo0;
-      for (int a = 0; a < 2; ++a)
-        for (int side = 0; side < 2; ++side) {
-          const srj_face_rule &b = d.bc[a][side];
-          p.bc_kind[a][side] = b.kind;
-          const bool arr = b.kind == SRJ_BC_FACE_DIRICHLET && b.values;
-          p.bc_ptr[a][side] = arr ? b.values : plan->bc_scalars + 2 * a + side;
-          p.bc_step[a][side] = arr ? 1 : 0;
-        }
-      CUtensorMap tu, tf;
-      int rc = make_tmap(&tu, cur, l, k2.box_cols);
-      if (rc != SRJ_OK) return rc;
-      rc = make_tmap(&tf, f, l, k2.box_cols);
-      if (rc != SRJ_OK) return rc;
-      const int warps = p.nbands * p.nstrips;
-      const int blocks = (warps + Band2D<1, 2>::WARPS - 1) / Band2D<1, 2>::WARPS;
-      k2.launch(p, tu, tf, blocks, st);
-    } else if (t > 1) {
-      // temporally blocked 3D (constant stencil): t fused sweeps per launch
-      Sweep3DTBParams p{};
-      p.dst = nxt + ioff;
-      for (int a = 0; a < 7; ++a) p.kc[a] = d.coef[a];
-      p.kinv = recip_or_zero(d.coef[0]);
-      p.kinv_lo = recip_lo(d.coef[0], p.kinv);
-      p.pitch = l.pitch;
-      p.plane = l.plane;
-      p.n0 = int(l.n[0]);
-      p.n1 = int(l.n[1]);
-      p.n2 = int(l.n[2]);
-      p.ld_lo = ld_lo;
-      p.ld_hi = ld_hi;
-      p.own_b = int(d.own0_begin);
-      p.own_e = int(d.own0_end);
-      p.tma_col0 = int(l.origin + 1);
-      p.rows_per_plane = int(l.n[1] + 2);
-      p.tma_row0 = l.halo0 * p.rows_per_plane + 1;  // row of (i=0, j=0)
-      for (int q = 0; q < t; ++q) p.omega[q] = weights[(first + k + q) % m];
-      p.norms = d_norms + 2 * k;
-      for (int a = 0; a < 3; ++a)
-        for (int side = 0; side < 2; ++side) {
-          const srj_face_rule &b = d.bc[a][side];
-          p.bc_kind[a][side] = b.kind;
-          const bool arr = b.kind == SRJ_BC_FACE_DIRICHLET && b.values;
-          p.bc_ptr[a][side] = arr ? b.values : plan->bc_scalars + 2 * a + side;
-          p.bc_step[a][side] = arr ? 1 : 0;
-        }
-      int bcf = 0;
-      if (plan->has_bc) {
-        bcf = 2;
-        for (int a = 0; a < 3; ++a)
-          for (int side = 0; side < 2; ++side)
-            if (d.bc[a][side].kind == SRJ_BC_FACE_DIRICHLET) bcf = 1;
-      }
-      const Kernel3DTB k3 = pick3d_tb(t, nl, p.kinv != 0.0, bcf);
-      p.ntj = int((l.n[1] + k3.tj - 1) / k3.tj);
-      p.ntk = int((l.n[2] + k3.tk - 1) / k3.tk);
-      const long tiles = long(p.ntj) * p.ntk;
-      const long capacity = long(sm_count()) * k3.blocks_per_sm();
-      int nstrips = 1;
-      double best = -1.0;
-      for (int ns = 1; ns <= std::max(1, std::min(64, rows / (4 * t))); ++ns) {
-        const long w = tiles * ns;
-        const long waves = (w + capacity - 1) / capacity;
-        const double hh = double(rows) / ns;
-        const double eff = double(w) / double(waves * capacity) * hh / (hh + 2.0 * t);
-        if (eff > best + 1e-9) {
-          best = eff;
-          nstrips = ns;
-        }
-      }
-      p.H = (rows + nstrips - 1) / nstrips;
-      p.nstrips = (rows + p.H - 1) / p.H;
-      CUtensorMap tu, tf;
-      int rc = make_tmap(&tu, cur, l, k3.box_cols, k3.box_rows);
-      if (rc != SRJ_OK) return rc;
-      rc = make_tmap(&tf, f, l, k3.box_cols, k3.box_rows);
-      if (rc != SRJ_OK) return rc;
-      k3.launch(p, tu, tf, int(tiles * p.nstrips), st);
-    } else {
-      Sweep3DParams p{};
-      p.src = cur + ioff;
-      p.dst = nxt + ioff;
-      p.f = f + ioff;
-      p.act = d.act ? d.act + ioff : nullptr;
-      for (int a = 0; a < 7; ++a) {
-        p.coef[a] = var ? d.coef_arrays[a] + ioff : nullptr;
-        p.kc[a] = d.coef[a];
-      }
-      p.pitch = l.pitch;
-      p.plane = l.plane;
-      p.n0 = int(l.n[0]);
-      p.n1 = int(l.n[1]);
-      p.n2 = int(l.n[2]);
-      // one-deep stencil: only owned rows relax; exchanged halos are inputs
-      p.lo_c = 0;
-      p.hi_c = p.n0;
-      p.ld_lo = ld_lo;
-      p.ld_hi = ld_hi;
-      p.own_b = int(d.own0_begin);
-      p.own_e = int(d.own0_end);
-      p.nbands = int((l.n[2] + 63) / 64);
-      p.njg = int((l.n[1] + kRows3D - 1) / kRows3D);
-      p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
-      p.kinv_lo = recip_lo(d.coef[0], p.kinv);
-      const bool recip = !var && p.kinv != 0.0;
-      const Kernel3D k3 = pick3d(var, nl, recip);
-      const long per_strip = long(p.njg) * p.nbands;
-      const long capacity = long(sm_count()) * k3.blocks_per_sm() * kWarps3D;
-      // strips: best fill of whole waves, discounting the 2 halo planes per strip
-      int nstrips = 1;
-      double best = -1.0;
-      for (int ns = 1; ns <= std::max(1, std::min(64, rows / 8)); ++ns) {
-        const long w = per_strip * ns;
-        const long waves = (w + capacity - 1) / capacity;
-        const double hh = double(rows) / ns;
-        const double eff = double(w) / double(waves * capacity) * hh / (hh + 2.0);
-        if (eff > best + 1e-9) {
-          best = eff;
-          nstrips = ns;
-        }
-      }
-      p.H = (rows + nstrips - 1) / nstrips;
-      p.nstrips = (rows + p.H - 1) / p.H;
-      p.omega = weights[(first + k) % m];
-      p.norms = d_norms + 2 * k;
-      const long warps = per_strip * p.nstrips;
-      k3.launch(p, int((warps + kWarps3D - 1) / kWarps3D), st);
-    }
-    SRJ_CUDA(cudaGetLastError());
+    double om[kMaxFuse];
+    for (int q = 0; q < t; ++q) om[q] = weights[(first + k + q) % m];
+    int rc = launch_fused(*plan, d.own0_begin, d.own0_end, cur, nxt, om, t, d_norms + 2 * k, st);
+    if (rc != SRJ_OK) return rc;
     if (plan->has_bc) {
-      const int rc = launch_ghosts(d, nxt + ioff, st);
+      rc = launch_ghosts(d, nxt + ioff, st);
       if (rc != SRJ_OK) return rc;
     }
     if (plan->g_n > 0) {
-      const int rc = launch_gather(*plan, nxt, st);
+      rc = launch_gather(*plan, nxt, st);
       if (rc != SRJ_OK) return rc;
     }
     k += t;

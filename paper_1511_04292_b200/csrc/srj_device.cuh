@@ -106,7 +106,7 @@ __device__ __forceinline__ bool recip_unsafe(double a) {
 
 // out of line: the IEEE division is the rare path and its inline expansion
 // would triple the size of the unrolled fast loop
-__device__ __noinline__ double div_ieee(double a, double c) { return __ddiv_rn(a, c); }
+static __device__ __noinline__ double div_ieee(double a, double c) { return __ddiv_rn(a, c); }
 
 // keep the entry of larger magnitude (signed); NaN never replaces m
 __device__ __forceinline__ void acc_absmax(double &m, double x) {

@@ -20,7 +20,9 @@
 // consecutive sweeps pipeline; every strip is co-resident (cooperative
 // launch), and the waits only point to earlier rows in this sweep or later
 // rows in the previous one, so they cannot deadlock.  Operands are loaded
-// five steps ahead (register ring); right and down come from the ring.  Per-cell arithmetic and the masks are the reference's.
+// kPF steps ahead into a register ring (kPF = 14 in 2D / 6 in 3D for constant
+// stencils when every strip fits at that occupancy, else 4); right and down
+// come from the ring.  Per-cell arithmetic and the masks are the reference's.
 #pragma once
 #include "srj_device.cuh"
 
@@ -79,7 +81,7 @@ __device__ __forceinline__ unsigned long long wait_ge(const unsigned long long *
   return have;
 }
 
-template <int ND, bool VAR, bool RECIP>
+template <int ND, bool VAR, bool RECIP, bool DEEP>
 __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams p) {
   const int lane = threadIdx.x;
   const int s = blockIdx.x;
@@ -132,8 +134,11 @@ __global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams 
   };
   // ring depth: deeper rings hide more of the per-step latency (4096^2:
   // kPF 4 / 6 / 9 / 14 -> 9.9 / 10.8 / 11.8 / 12.4 GLUPS) within 255
-  // registers (2D constant 240-250; the 3D and per-cell rings hold more)
-  constexpr int kPF = VAR ? 4 : (ND == 2 ? 14 : 6);
+  // registers (2D constant 240-250; the 3D and per-cell rings hold more).
+  // The deep rings cost occupancy (8 co-resident warps per SM instead of
+  // ~12): grids whose strips do not all fit then take the DEEP=false copy
+  // (kPF 4), chosen at launch from the occupancy query (srj_capi.cu launch_gs)
+  constexpr int kPF = (VAR || !DEEP) ? 4 : (ND == 2 ? 14 : 6);
 
 #pragma unroll 1
   for (int k = 0; k < p.nsweeps; ++k) {

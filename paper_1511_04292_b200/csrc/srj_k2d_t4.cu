@@ -1,0 +1,6 @@
+// Instantiates the 2D band kernel for fused depth(s) 4 (see srj_k2d_impl.cuh).
+#include "srj_k2d_impl.cuh"
+
+namespace srj_host {
+template Kernel2D pick2d_t<4>(bool, bool, bool, int);
+}  // namespace srj_host

@@ -88,9 +88,12 @@ class DeviceGrid:
             self._keep = []
             self.fields = [torch.zeros(elems, dtype=torch.float64, device=self.device)
                            for _ in range(3)]
-            host_u = _contig(u, np.float64)
-            for f in self.fields:
-                self.upload_field(host_u, f)
+            # one host->device copy; the other two buffers (whose ghost layers
+            # the kernels never write) are device copies of it
+            self.upload_field(_contig(u, np.float64), self.fields[0])
+            with torch.cuda.stream(self.stream):
+                for f in self.fields[1:]:
+                    f.copy_(self.fields[0])
 
             desc = _lib.SrjPlanDesc()
             desc.layout = self.layout

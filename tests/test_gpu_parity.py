@@ -763,27 +763,65 @@ def test_gauss_seidel_wavefront_short_planes():
         assert np.array_equal(hist.true_residual_inf, norms[:, 1]), shape
 
 
+def _gs_fields(rng, shape, constant):
+    nd = len(shape)
+    if constant:  # constant stencil: the deep register rings (kPF 14 in 2D, 6 in 3D)
+        cen = np.full(shape, 2.0 * nd + 0.37)
+        lo = tuple(np.full(shape, -0.9 - 0.01 * a) for a in range(nd))
+        hi = tuple(np.full(shape, -0.8 + 0.01 * a) for a in range(nd))
+    else:
+        cen = 2.0 * nd + rng.random(shape)
+        lo = tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd))
+        hi = tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd))
+    return {"u": rng.standard_normal(tuple(n + 2 for n in shape)),
+            "source": rng.standard_normal(shape), "center": cen, "lower": lo, "upper": hi,
+            "mask": None}
+
+
+def _gs_check(f, omega, steps):
+    q = problem_from(f)
+    _, _, norms = oracle.gs_solve(q, omega, steps, sor=omega != 1.0)
+    p = problem_from(f)
+    if omega == 1.0:
+        hist, _ = G.gauss_seidel_solve(p, 1e-300, max_iters=steps)
+    else:
+        hist, _ = G.sor_solve(p, omega, 1e-300, max_iters=steps)
+    assert np.array_equal(p.u, q.u)
+    assert np.array_equal(hist.true_residual_inf, norms[:, 1])
+    assert np.array_equal(hist.residual_inf, norms[:, 0] / (omega if omega != 1.0 else 1.0))
+
+
+@pytest.mark.parametrize("constant", [False, True])
 @pytest.mark.parametrize("nd", [2, 3])
-def test_gauss_seidel_wavefront_narrow_rows(nd):
+def test_gauss_seidel_wavefront_narrow_rows(nd, constant):
     """Rows of 1..9 columns: each progress wait covers up to kPF+1 prefetched
     steps, so its requirement must stay monotone past the last column (a wait
     skipped there let lane 0 read the previous strip's row early -- random
     seeds 278 and 315 of test_gpu_random at SRJ_RANDOM_CASES=400).  Many short
-    strips keep neighbouring strips close in time, where a missing wait shows."""
-    rng = np.random.default_rng(13 + nd)
+    strips keep neighbouring strips close in time, where a missing wait shows.
+    ``constant`` runs the constant-stencil copies, whose deeper rings look
+    ahead up to 2*kPF+1 steps."""
+    rng = np.random.default_rng(13 + nd + 7 * constant)
     for ncols in range(1, 10 if nd == 2 else 7):
         shape = (3000, ncols) if nd == 2 else (40, 60, ncols)
-        f = {"u": rng.standard_normal(tuple(n + 2 for n in shape)),
-             "source": rng.standard_normal(shape), "center": 2.0 * nd + rng.random(shape),
-             "lower": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd)),
-             "upper": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd)), "mask": None}
+        f = _gs_fields(rng, shape, constant)
         for omega in (1.0, 1.3):
-            q = problem_from(f)
-            _, _, norms = oracle.gs_solve(q, omega, 12, sor=omega != 1.0)
-            p = problem_from(f)
-            if omega == 1.0:
-                hist, _ = G.gauss_seidel_solve(p, 1e-300, max_iters=12)
-            else:
-                hist, _ = G.sor_solve(p, omega, 1e-300, max_iters=12)
-            assert np.array_equal(p.u, q.u), (shape, omega)
-            assert np.array_equal(hist.true_residual_inf, norms[:, 1]), (shape, omega)
+            _gs_check(f, omega, 12)
+
+
+@pytest.mark.parametrize("shape", [(2000, 300), (12, 40, 50), (30, 2, 80)])
+def test_gauss_seidel_deep_ring_many_strips(shape):
+    """Constant stencils with many strips and short planes on the deep rings."""
+    rng = np.random.default_rng(sum(shape))
+    _gs_check(_gs_fields(rng, shape, True), 1.0, 9)
+    _gs_check(_gs_fields(rng, shape, True), 1.6, 7)
+
+
+@pytest.mark.parametrize("rows", [40_000, 45_000])
+def test_gauss_seidel_beyond_deep_ring_occupancy(rows):
+    """(i, j) row counts above what the deep constant-stencil ring can hold
+    co-resident (148 SMs x 8 warps x 32 rows = 37,888) run on the kPF=4 copy
+    instead of raising (3-D 200^3 has 40,000 rows)."""
+    rng = np.random.default_rng(rows)
+    shape = (rows // 200, 200, 24)
+    _gs_check(_gs_fields(rng, shape, True), 1.0, 3)
