@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SRJ_ABI_VERSION 4
+#define SRJ_ABI_VERSION 5
 
 enum {
     SRJ_OK = 0,
@@ -177,6 +177,15 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a,
 int srj_plan_residual(srj_plan *plan, const double *u, double *d_out,
                       void *stream);
 
+/* Per-layer true residual: d_layers[2*(i - own0_begin) + {0, 1}] = (sum r^2,
+ * max |r|) over the owned active cells of axis-0 layer i (2D: a row, 3D: a
+ * plane), for every owned layer i (GridProblem.residual_field,
+ * grids.py:249-266).  A layer's value depends only on its cells (fixed
+ * reduction order per layer), so a host sum over layers is independent of how
+ * the grid is split across GPUs.  d_layers: device, 2*(own0_end-own0_begin). */
+int srj_plan_residual_layers(srj_plan *plan, const double *u, double *d_layers,
+                             void *stream);
+
 /* Gauss-Seidel / SOR: `nsweeps` in-place lexicographic sweeps of field `u`
  * (a buffer in the plan's layout) with relaxation factor omega (1 = GS),
  * bitwise the reference's _gs2 / _gs3 (grids.py:426-474) followed by its ghost
@@ -208,6 +217,69 @@ int srj_upload_interior(const srj_layout_t *lay, const void *host, void *dev,
 int srj_copy_layers(const srj_layout_t *lay, const double *src,
                     int64_t src_layer, double *dst, int64_t dst_layer,
                     int64_t count, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Slab decomposition across GPUs (the reference has no parallel
+ * path -- SPEC.md:305 -- and relies on Jacobi's insensitivity to domain
+ * decomposition).  Each rank owns a block of axis-0 rows of
+ * the global grid plus `halo` >= fuse exchanged rows per neighbour side, held
+ * as interior rows of its local plan (desc.own0_begin/end = the owned rows).
+ * srj_slab_run replaces the per-step loop of _iterate/_Sweeper.jacobi
+ * (grids.py:613-617, :544-559) for one rank: per fused launch it relaxes the
+ * edge rows, copies them into the neighbours' halo rows of the destination
+ * buffer over NVLink (peer cudaMemcpyAsync on a side stream), and relaxes the
+ * inner rows meanwhile.  Ranks order each other on the device through flag
+ * words in each other's memory (stream memory operations: wait for "halo of
+ * my source delivered" before the edge launch, "neighbour finished reading
+ * the buffer I write into" before the copy), so the host only enqueues work.
+ * ------------------------------------------------------------------------ */
+#define SRJ_SLAB_FLAG_WORDS 8   /* uint32 flag words per rank (device)       */
+
+typedef struct srj_slab srj_slab;
+
+typedef struct {
+    double *bufs[3];     /* the neighbour's three field buffers, addressable
+                            from this rank's device (IPC-mapped peer memory,
+                            or the same device when ranks are emulated)      */
+    uint32_t *flags;     /* the neighbour's flag block                        */
+    int64_t dst_row;     /* neighbour-local interior row where the rows this
+                            rank sends land (lower neighbour: its own0_end;
+                            upper neighbour: 0)                               */
+} srj_slab_peer;
+
+/* desc: the rank's local plan (FIXED faces only); bufs: its three field
+ * buffers (the same three every srj_slab_run call uses by index); flags:
+ * SRJ_SLAB_FLAG_WORDS device words; has_lo/has_hi: neighbours exist. */
+int srj_slab_create(const srj_plan_desc *desc, int32_t halo, double *const *bufs,
+                    uint32_t *flags, int32_t has_lo, int32_t has_hi,
+                    srj_slab **out);
+/* side 0 = lower neighbour (rank-1), 1 = upper (rank+1). */
+int srj_slab_connect(srj_slab *slab, int32_t side, const srj_slab_peer *peer);
+/* Zero this rank's flags and launch counter (all ranks, then a host barrier,
+ * before the first srj_slab_run). */
+int srj_slab_reset(srj_slab *slab, void *stream);
+int srj_slab_destroy(srj_slab *slab);
+/* The slab's plan (for srj_plan_residual_layers etc.; owned by the slab). */
+srj_plan *srj_slab_plan(srj_slab *slab);
+/* Steps first .. first+nsteps-1 (omega_k = weights[k mod m]) from field buffer
+ * `src` (0..2, left untouched) ping-ponging over the other two; *final_buf =
+ * the buffer index holding the result.  d_norms[i]: device, 2*nsteps doubles
+ * of per-step (dmax, rmax) over slab i's owned rows (MAX over ranks is the
+ * caller's all-reduce).  n > 1 slabs in one call = ranks emulated on one
+ * device, all enqueued on streams[0] in dependency order; n == 1: this
+ * process's rank on streams[0] (+ an internal comm stream). */
+int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src,
+                 const double *weights, int64_t m, int64_t first, int64_t nsteps,
+                 int32_t fuse, double *const *d_norms, int32_t *final_buf,
+                 void *const *streams);
+
+/* CUDA IPC between the ranks' processes: handle (64 bytes) + byte offset of
+ * dev_ptr inside its allocation; srj_ipc_open maps it (peer access enabled
+ * lazily) and returns the address of the same byte; srj_ipc_close unmaps
+ * (pass ptr - offset, the mapped base). */
+int srj_ipc_get_handle(const void *dev_ptr, void *handle, int64_t *offset);
+int srj_ipc_open(const void *handle, int64_t offset, void **dev_ptr);
+int srj_ipc_close(void *base);
 
 /* Diagnostic: out[i] = a[i]/c through the reciprocal-refinement division the
  * constant-stencil kernels use (y = RN(1/c), two Markstein corrections), and

@@ -8,7 +8,8 @@ build command.  ``load()`` is the single gate.
 import ctypes
 import os
 
-__all__ = ["BC_KINDS", "LIB_PATH", "SrjFaceRule", "SrjLayout", "SrjPlanDesc", "check", "load"]
+__all__ = ["BC_KINDS", "LIB_PATH", "SrjFaceRule", "SrjLayout", "SrjPlanDesc", "SrjSlabPeer",
+           "check", "load"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsrj.so")
 
@@ -17,7 +18,8 @@ SRJ_EINVAL = -1
 SRJ_ECUDA = -2
 SRJ_ENOMEM = -3
 SRJ_EUNSUPPORTED = -4
-ABI_VERSION = 4
+ABI_VERSION = 5
+SLAB_FLAG_WORDS = 8
 
 BC_KINDS = {"fixed": 0, "mirror": 1, "periodic": 2, "face_dirichlet": 3}
 
@@ -62,6 +64,14 @@ class SrjPlanDesc(ctypes.Structure):
     ]
 
 
+class SrjSlabPeer(ctypes.Structure):
+    _fields_ = [
+        ("bufs", ctypes.c_void_p * 3),
+        ("flags", ctypes.c_void_p),
+        ("dst_row", ctypes.c_int64),
+    ]
+
+
 _LIB = None
 
 _SIGNATURES = {
@@ -86,6 +96,28 @@ _SIGNATURES = {
                                     ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p]),
     "srj_plan_residual": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p]),
+    "srj_plan_residual_layers": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_void_p]),
+    "srj_slab_create": (ctypes.c_int, [ctypes.POINTER(SrjPlanDesc), ctypes.c_int32,
+                                       ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p,
+                                       ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.POINTER(ctypes.c_void_p)]),
+    "srj_slab_connect": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32,
+                                        ctypes.POINTER(SrjSlabPeer)]),
+    "srj_slab_reset": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "srj_slab_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "srj_slab_plan": (ctypes.c_void_p, [ctypes.c_void_p]),
+    "srj_slab_run": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                    ctypes.c_int32, _c_dp, ctypes.c_int64, ctypes.c_int64,
+                                    ctypes.c_int64, ctypes.c_int32,
+                                    ctypes.POINTER(ctypes.c_void_p),
+                                    ctypes.POINTER(ctypes.c_int32),
+                                    ctypes.POINTER(ctypes.c_void_p)]),
+    "srj_ipc_get_handle": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.POINTER(ctypes.c_int64)]),
+    "srj_ipc_open": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64,
+                                    ctypes.POINTER(ctypes.c_void_p)]),
+    "srj_ipc_close": (ctypes.c_int, [ctypes.c_void_p]),
     "srj_plan_gs": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                    ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "srj_upload_field": (ctypes.c_int, [ctypes.POINTER(SrjLayout), ctypes.c_void_p,

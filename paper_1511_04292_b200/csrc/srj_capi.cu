@@ -211,6 +211,8 @@ struct srj_plan {
   bool bc_fusable;   // ...and none is PERIODIC: fused launches form the ghosts on chip
   int default_fuse;
   double *partials;  // [kResidBlocks][2] device scratch
+  double *row_parts = nullptr;  // 3D per-(i,j)-row residual partials (srj_plan_residual_layers)
+  int64_t row_parts_cap = 0;
   double *bc_scalars;  // [3][2] device copies of the faces' scalar values (fused BCs)
   // small-grid cluster path: per-chunk omegas (device + pinned staging)
   double *d_omegas = nullptr, *h_omegas = nullptr;
@@ -458,6 +460,7 @@ int srj_plan_destroy(srj_plan *p) {
   free_gather(p);
   if (p->gs_prog) cudaFree(p->gs_prog);
   if (p->partials) cudaFree(p->partials);
+  if (p->row_parts) cudaFree(p->row_parts);
   if (p->bc_scalars) cudaFree(p->bc_scalars);
   if (p->d_omegas) cudaFree(p->d_omegas);
   if (p->h_omegas) cudaFreeHost(p->h_omegas);
@@ -897,6 +900,74 @@ static int plan_depth(const srj_plan &plan, int fuse) {
   return T;
 }
 
+// ------------------------------------------------------- slab exchange
+// Driver entry points (no -lcuda): stream memory operations order the halo
+// exchange between ranks on the device, with no host round trip per launch.
+struct DriverOps {
+  PFN_cuStreamWaitValue32_v11070 wait32 = nullptr;
+  PFN_cuStreamWriteValue32_v11070 write32 = nullptr;
+  PFN_cuMemGetAddressRange_v3020 addr_range = nullptr;
+  bool ok = false;
+};
+
+static const DriverOps &driver_ops() {
+  static DriverOps ops;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *a = nullptr, *b = nullptr, *c = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2, q3;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &a, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWriteValue32", &b, cudaEnableDefault, &q2) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuMemGetAddressRange", &c, cudaEnableDefault, &q3) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess &&
+        q3 == cudaDriverEntryPointSuccess) {
+      ops.wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(a);
+      ops.write32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(b);
+      ops.addr_range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(c);
+      ops.ok = true;
+    }
+    cudaGetLastError();
+  });
+  return ops;
+}
+
+// flag words of a rank's block (written by its neighbours)
+enum { kFlagArrived = 0, kFlagDone = 2 };  // + side (0 = from the lower, 1 = from the upper neighbour)
+
+struct srj_slab {
+  srj_plan *plan = nullptr;   // the rank's plan (owned rows = desc own range)
+  double *bufs[3] = {};
+  uint32_t *flags = nullptr;  // SRJ_SLAB_FLAG_WORDS words, device
+  int halo = 1;
+  bool has[2] = {false, false};
+  srj_slab_peer peer[2] = {};
+  uint32_t epoch = 0;         // launches run since the last reset (all ranks agree)
+  int device = 0;
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_edge = nullptr, ev_copy = nullptr;
+  // local interior row ranges: edges (sent after every launch) and inner
+  int64_t part_b[3] = {}, part_e[3] = {};  // [0] lower edge, [1] upper edge, [2] inner (empty: b == e)
+};
+
+static int slab_wait(cudaStream_t st, uint32_t *addr, uint32_t v) {
+  const CUresult r = driver_ops().wait32(reinterpret_cast<CUstream>(st), CUdeviceptr(addr), v,
+                                         CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(SRJ_ECUDA, "cuStreamWaitValue32 failed (%d)", int(r));
+  return SRJ_OK;
+}
+
+static int slab_write(cudaStream_t st, uint32_t *addr, uint32_t v) {
+  const CUresult r = driver_ops().write32(reinterpret_cast<CUstream>(st), CUdeviceptr(addr), v,
+                                          CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return fail(SRJ_ECUDA, "cuStreamWriteValue32 failed (%d)", int(r));
+  return SRJ_OK;
+}
+
+// element offset of local interior row `row` (layer row + halo0) in a field buffer
+static int64_t layer_offset(const srj_layout_t &l, int64_t row) {
+  return l.origin + (row + l.halo0) * l.plane;
+}
+
 extern "C" {
 
 int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b,
@@ -952,9 +1023,8 @@ int srj_plan_run(srj_plan *plan, const double *src, double *buf_a, double *buf_b
   return SRJ_OK;
 }
 
-int srj_plan_residual(srj_plan *plan, const double *u, double *d_out, void *stream) {
-  if (!plan || !u || !d_out) return fail(SRJ_EINVAL, "null argument");
-  const srj_plan_desc &d = plan->d;
+static ResidParams resid_params(const srj_plan &plan, const double *u) {
+  const srj_plan_desc &d = plan.d;
   const srj_layout_t &l = d.layout;
   const int64_t ioff = interior_offset(l);
   ResidParams p{};
@@ -975,7 +1045,15 @@ int srj_plan_residual(srj_plan *plan, const double *u, double *d_out, void *stre
   p.n2 = (l.ndim == 3) ? int(l.n[2]) : 1;
   p.own_b = int(d.own0_begin);
   p.own_e = int(d.own0_end);
-  p.partials = plan->partials;
+  p.partials = plan.partials;
+  return p;
+}
+
+int srj_plan_residual(srj_plan *plan, const double *u, double *d_out, void *stream) {
+  if (!plan || !u || !d_out) return fail(SRJ_EINVAL, "null argument");
+  const srj_plan_desc &d = plan->d;
+  const ResidParams p = resid_params(*plan, u);
+  const bool nl = d.kappa != nullptr, var = d.coef_mode == 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (var)
     nl ? residual_partial<true, true><<<kResidBlocks, kResidThreads, 0, st>>>(p)
@@ -984,6 +1062,42 @@ int srj_plan_residual(srj_plan *plan, const double *u, double *d_out, void *stre
     nl ? residual_partial<false, true><<<kResidBlocks, kResidThreads, 0, st>>>(p)
        : residual_partial<false, false><<<kResidBlocks, kResidThreads, 0, st>>>(p);
   residual_final<<<1, 32, 0, st>>>(plan->partials, kResidBlocks, d_out);
+  SRJ_CUDA(cudaGetLastError());
+  return SRJ_OK;
+}
+
+int srj_plan_residual_layers(srj_plan *plan, const double *u, double *d_layers, void *stream) {
+  if (!plan || !u || !d_layers) return fail(SRJ_EINVAL, "null argument");
+  const srj_plan_desc &d = plan->d;
+  const srj_layout_t &l = d.layout;
+  const ResidParams p = resid_params(*plan, u);
+  const bool nl = d.kappa != nullptr, var = d.coef_mode == 1;
+  const int64_t layers = d.own0_end - d.own0_begin;
+  if (layers <= 0) return SRJ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double *rows_out = d_layers;
+  if (l.ndim == 3) {
+    const int64_t need = 2 * layers * l.n[1];
+    if (need > plan->row_parts_cap) {
+      if (plan->row_parts) cudaFree(plan->row_parts);  // implicit device sync (first use)
+      plan->row_parts = nullptr;
+      plan->row_parts_cap = 0;
+      SRJ_CUDA(cudaMalloc(&plan->row_parts, sizeof(double) * size_t(need)));
+      plan->row_parts_cap = need;
+    }
+    rows_out = plan->row_parts;
+  }
+  const int blocks = sm_count() * 8;  // 64 warps per SM, grid-stride over rows
+  if (var)
+    nl ? residual_rows<true, true><<<blocks, 256, 0, st>>>(p, rows_out)
+       : residual_rows<true, false><<<blocks, 256, 0, st>>>(p, rows_out);
+  else
+    nl ? residual_rows<false, true><<<blocks, 256, 0, st>>>(p, rows_out)
+       : residual_rows<false, false><<<blocks, 256, 0, st>>>(p, rows_out);
+  if (l.ndim == 3) {
+    const int lb = int(std::min<int64_t>((layers + 7) / 8, int64_t(sm_count()) * 4));
+    residual_layers<<<lb, 256, 0, st>>>(plan->row_parts, int(layers), int(l.n[1]), d_layers);
+  }
   SRJ_CUDA(cudaGetLastError());
   return SRJ_OK;
 }
@@ -1108,6 +1222,225 @@ int srj_copy_layers(const srj_layout_t *lay, const double *src, int64_t src_laye
   SRJ_CUDA(cudaMemcpyAsync(dst + l.origin + dst_layer * l.plane, src + l.origin + src_layer * l.plane,
                            sizeof(double) * size_t(count * l.plane), cudaMemcpyDefault,
                            static_cast<cudaStream_t>(stream)));
+  return SRJ_OK;
+}
+
+/* ------------------------------------------------------------ slab API */
+
+int srj_slab_create(const srj_plan_desc *desc, int32_t halo, double *const *bufs, uint32_t *flags,
+                    int32_t has_lo, int32_t has_hi, srj_slab **out) {
+  if (!desc || !bufs || !flags || !out) return fail(SRJ_EINVAL, "null argument");
+  if (!bufs[0] || !bufs[1] || !bufs[2]) return fail(SRJ_EINVAL, "null field buffer");
+  if (halo < 1 || halo > kMaxFuse) return fail(SRJ_EINVAL, "halo must be in [1, %d]", kMaxFuse);
+  if (!driver_ops().ok) return fail(SRJ_EUNSUPPORTED, "CUDA stream memory operations unavailable");
+  srj_plan *plan = nullptr;
+  int rc = srj_plan_create(desc, &plan);
+  if (rc != SRJ_OK) return rc;
+  if (plan->has_bc || plan->g_n > 0) {
+    srj_plan_destroy(plan);
+    return fail(SRJ_EUNSUPPORTED, "slab decomposition supports FIXED faces only");
+  }
+  const int64_t ob = plan->d.own0_begin, oe = plan->d.own0_end;
+  const int64_t n0 = plan->d.layout.n[0];
+  if ((has_lo && ob < halo) || (has_hi && n0 - oe < halo) || oe - ob < halo) {
+    srj_plan_destroy(plan);
+    return fail(SRJ_EINVAL, "owned rows [%lld, %lld) of %lld leave no room for %d halo rows",
+                (long long)ob, (long long)oe, (long long)n0, halo);
+  }
+  srj_slab *sl = new (std::nothrow) srj_slab;
+  if (!sl) {
+    srj_plan_destroy(plan);
+    return fail(SRJ_ENOMEM, "host allocation failed");
+  }
+  sl->plan = plan;
+  for (int i = 0; i < 3; ++i) sl->bufs[i] = bufs[i];
+  sl->flags = flags;
+  sl->halo = halo;
+  sl->has[0] = has_lo != 0;
+  sl->has[1] = has_hi != 0;
+  sl->device = current_device();
+  const int64_t a = ob + (sl->has[0] ? halo : 0), b = oe - (sl->has[1] ? halo : 0);
+  if (a >= b) {  // thin slab: one edge launch covers every owned row
+    sl->part_b[0] = ob;
+    sl->part_e[0] = oe;
+    sl->part_b[1] = sl->part_e[1] = sl->part_b[2] = sl->part_e[2] = 0;
+  } else {
+    sl->part_b[0] = ob;
+    sl->part_e[0] = a;
+    sl->part_b[1] = b;
+    sl->part_e[1] = oe;
+    sl->part_b[2] = a;
+    sl->part_e[2] = b;
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&sl->comm, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl->ev_edge, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl->ev_copy, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    srj_slab_destroy(sl);
+    return cuda_fail(e, "slab stream/event creation");
+  }
+  *out = sl;
+  return SRJ_OK;
+}
+
+int srj_slab_connect(srj_slab *sl, int32_t side, const srj_slab_peer *peer) {
+  if (!sl || !peer || side < 0 || side > 1) return fail(SRJ_EINVAL, "bad argument");
+  if (!sl->has[side]) return fail(SRJ_EINVAL, "this slab has no neighbour on side %d", side);
+  if (!peer->bufs[0] || !peer->bufs[1] || !peer->bufs[2] || !peer->flags)
+    return fail(SRJ_EINVAL, "null peer pointer");
+  if (peer->dst_row < 0) return fail(SRJ_EINVAL, "negative peer row");
+  sl->peer[side] = *peer;
+  return SRJ_OK;
+}
+
+int srj_slab_reset(srj_slab *sl, void *stream) {
+  if (!sl) return fail(SRJ_EINVAL, "null slab");
+  SRJ_CUDA(cudaMemsetAsync(sl->flags, 0, sizeof(uint32_t) * SRJ_SLAB_FLAG_WORDS,
+                           static_cast<cudaStream_t>(stream)));
+  sl->epoch = 0;
+  return SRJ_OK;
+}
+
+int srj_slab_destroy(srj_slab *sl) {
+  if (!sl) return SRJ_OK;
+  if (sl->comm) cudaStreamDestroy(sl->comm);
+  if (sl->ev_edge) cudaEventDestroy(sl->ev_edge);
+  if (sl->ev_copy) cudaEventDestroy(sl->ev_copy);
+  if (sl->plan) srj_plan_destroy(sl->plan);
+  delete sl;
+  return SRJ_OK;
+}
+
+srj_plan *srj_slab_plan(srj_slab *sl) { return sl ? sl->plan : nullptr; }
+
+int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *weights, int64_t m,
+                 int64_t first, int64_t nsteps, int32_t fuse, double *const *d_norms,
+                 int32_t *final_buf, void *const *streams) {
+  if (!slabs || n < 1 || !weights || !d_norms || !final_buf || !streams)
+    return fail(SRJ_EINVAL, "null argument");
+  if (src < 0 || src > 2) return fail(SRJ_EINVAL, "src must be buffer 0, 1 or 2");
+  if (m < 1) return fail(SRJ_EINVAL, "weight cycle must be non-empty");
+  if (nsteps < 0 || first < 0) return fail(SRJ_EINVAL, "negative step range");
+  *final_buf = src;
+  if (nsteps == 0) return SRJ_OK;
+  // several slabs in one call (ranks emulated on one device): everything is
+  // enqueued on the one stream in dependency order, so every flag wait is
+  // already satisfied when the stream reaches it
+  const bool serial = n > 1;
+  int T = kMaxFuse;
+  for (int i = 0; i < n; ++i) {
+    srj_slab *sl = slabs[i];
+    if (!sl) return fail(SRJ_EINVAL, "null slab %d", i);
+    for (int sd = 0; sd < 2; ++sd)
+      if (sl->has[sd] && !sl->peer[sd].flags) return fail(SRJ_EINVAL, "slab %d is not connected", i);
+    T = std::min(T, plan_depth(*sl->plan, fuse));
+    if (T > sl->halo) T = sl->halo;
+    SRJ_CUDA(cudaMemsetAsync(d_norms[i], 0, sizeof(double) * 2 * size_t(nsteps),
+                             static_cast<cudaStream_t>(streams[serial ? 0 : i])));
+  }
+  const int others[3][2] = {{1, 2}, {0, 2}, {0, 1}};
+  int cur = src, flip = 0;
+  int64_t k = 0;
+  while (k < nsteps) {
+    const int t = int(std::min<int64_t>(T, nsteps - k));
+    const int dst = others[src][flip];
+    double om[kMaxFuse];
+    for (int q = 0; q < t; ++q) om[q] = weights[(first + k + q) % m];
+    // phase A: halo of `cur` delivered (previous launch) -> edge rows
+    for (int i = 0; i < n; ++i) {
+      srj_slab *sl = slabs[i];
+      cudaStream_t st = static_cast<cudaStream_t>(streams[serial ? 0 : i]);
+      for (int sd = 0; sd < 2; ++sd)
+        if (sl->has[sd]) {
+          const int rc = slab_wait(st, sl->flags + kFlagArrived + sd, sl->epoch);
+          if (rc != SRJ_OK) return rc;
+        }
+      for (int part = 0; part < 2; ++part)
+        if (sl->part_e[part] > sl->part_b[part]) {
+          const int rc = launch_fused(*sl->plan, sl->part_b[part], sl->part_e[part], sl->bufs[cur],
+                                      sl->bufs[dst], om, t, d_norms[i] + 2 * k, st);
+          if (rc != SRJ_OK) return rc;
+        }
+      if (!serial) SRJ_CUDA(cudaEventRecord(sl->ev_edge, st));
+    }
+    // phase B: send the edge rows into the neighbours' halo rows of `dst`
+    // once they finished every launch that read that buffer
+    for (int i = 0; i < n; ++i) {
+      srj_slab *sl = slabs[i];
+      if (!sl->has[0] && !sl->has[1]) continue;
+      cudaStream_t cs = serial ? static_cast<cudaStream_t>(streams[0]) : sl->comm;
+      if (!serial) SRJ_CUDA(cudaStreamWaitEvent(cs, sl->ev_edge, 0));
+      const srj_layout_t &l = sl->plan->d.layout;
+      for (int sd = 0; sd < 2; ++sd) {
+        if (!sl->has[sd]) continue;
+        const srj_slab_peer &pr = sl->peer[sd];
+        int rc = slab_wait(cs, sl->flags + kFlagDone + sd, sl->epoch);
+        if (rc != SRJ_OK) return rc;
+        const int64_t row = sd == 0 ? sl->plan->d.own0_begin : sl->plan->d.own0_end - sl->halo;
+        SRJ_CUDA(cudaMemcpyAsync(pr.bufs[dst] + layer_offset(l, pr.dst_row),
+                                 sl->bufs[dst] + layer_offset(l, row),
+                                 sizeof(double) * size_t(sl->halo * l.plane), cudaMemcpyDefault, cs));
+        // the neighbour sees this rank on its opposite side
+        rc = slab_write(cs, pr.flags + kFlagArrived + (1 - sd), sl->epoch + 1);
+        if (rc != SRJ_OK) return rc;
+      }
+      if (!serial) SRJ_CUDA(cudaEventRecord(sl->ev_copy, cs));
+    }
+    // phase C: inner rows while the halo rows travel; then tell the
+    // neighbours this launch (and its reads of `cur`) is complete
+    for (int i = 0; i < n; ++i) {
+      srj_slab *sl = slabs[i];
+      cudaStream_t st = static_cast<cudaStream_t>(streams[serial ? 0 : i]);
+      if (sl->part_e[2] > sl->part_b[2]) {
+        const int rc = launch_fused(*sl->plan, sl->part_b[2], sl->part_e[2], sl->bufs[cur],
+                                    sl->bufs[dst], om, t, d_norms[i] + 2 * k, st);
+        if (rc != SRJ_OK) return rc;
+      }
+      for (int sd = 0; sd < 2; ++sd)
+        if (sl->has[sd]) {
+          const int rc = slab_write(st, sl->peer[sd].flags + kFlagDone + (1 - sd), sl->epoch + 1);
+          if (rc != SRJ_OK) return rc;
+        }
+      // the next launches overwrite rows the copy of this one reads
+      if (!serial && (sl->has[0] || sl->has[1])) SRJ_CUDA(cudaStreamWaitEvent(st, sl->ev_copy, 0));
+      sl->epoch += 1;
+    }
+    k += t;
+    cur = dst;
+    flip ^= 1;
+  }
+  *final_buf = cur;
+  return SRJ_OK;
+}
+
+/* IPC: export a device allocation to another process of the same node */
+int srj_ipc_get_handle(const void *dev_ptr, void *handle, int64_t *offset) {
+  if (!dev_ptr || !handle || !offset) return fail(SRJ_EINVAL, "null argument");
+  if (!driver_ops().ok) return fail(SRJ_EUNSUPPORTED, "CUDA driver entry points unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  const CUresult r = driver_ops().addr_range(&base, &size, CUdeviceptr(dev_ptr));
+  if (r != CUDA_SUCCESS) return fail(SRJ_ECUDA, "cuMemGetAddressRange failed (%d)", int(r));
+  cudaIpcMemHandle_t h;
+  SRJ_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = int64_t(CUdeviceptr(dev_ptr) - base);
+  return SRJ_OK;
+}
+
+int srj_ipc_open(const void *handle, int64_t offset, void **dev_ptr) {
+  if (!handle || !dev_ptr || offset < 0) return fail(SRJ_EINVAL, "bad argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void *base = nullptr;
+  SRJ_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr = static_cast<char *>(base) + offset;
+  return SRJ_OK;
+}
+
+int srj_ipc_close(void *base) {
+  if (!base) return fail(SRJ_EINVAL, "null argument");
+  SRJ_CUDA(cudaIpcCloseMemHandle(base));
   return SRJ_OK;
 }
 

@@ -7,14 +7,14 @@ namespace srj_host {
 // cooperative launch (every strip co-resident).  The deep operand ring
 // (DEEP) is used when every strip fits at its occupancy, else the kPF=4 copy
 template <int ND, bool VAR, bool RECIP, bool DEEP>
-static int gs_fits(int nstrips) {
+static int gs_per_sm() {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_sweep<ND, VAR, RECIP, DEEP>, 32, 0) !=
       cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
-  return long(per_sm) * sm_count() >= nstrips;
+  return per_sm;
 }
 
 template <int ND, bool VAR, bool RECIP, bool DEEP>
@@ -30,9 +30,10 @@ static int launch_gs_t(const GSParams &p, int nstrips, cudaStream_t st) {
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, gs_sweep<ND, VAR, RECIP, DEEP>, p);
   if (e == cudaErrorCooperativeLaunchTooLarge) {
-    cudaGetLastError();  // clear the sticky-free launch error so later checks see none
+    cudaGetLastError();  // clear the launch error so later checks do not see it
     return fail(SRJ_EUNSUPPORTED, "Gauss-Seidel wavefront needs %d co-resident strips of 32 rows; "
-                "the grid has too many rows for one GPU", nstrips);
+                "the grid has too many rows for one GPU (%d warps per SM x %d SMs)", nstrips,
+                gs_per_sm<ND, VAR, RECIP, DEEP>(), sm_count());
   }
   SRJ_CUDA(e);
   return SRJ_OK;
@@ -41,7 +42,10 @@ static int launch_gs_t(const GSParams &p, int nstrips, cudaStream_t st) {
 template <int ND, bool VAR, bool RECIP>
 static int launch_gs_pick(const GSParams &p, int nstrips, cudaStream_t st) {
   if constexpr (!VAR) {
-    if (gs_fits<ND, VAR, RECIP, true>(nstrips)) return launch_gs_t<ND, VAR, RECIP, true>(p, nstrips, st);
+    if (long(gs_per_sm<ND, VAR, RECIP, true>()) * sm_count() >= nstrips) {
+      const int rc = launch_gs_t<ND, VAR, RECIP, true>(p, nstrips, st);
+      if (rc != SRJ_EUNSUPPORTED) return rc;  // else retry with the shallow ring
+    }
   }
   return launch_gs_t<ND, VAR, RECIP, false>(p, nstrips, st);
 }

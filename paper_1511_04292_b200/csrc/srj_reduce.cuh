@@ -113,6 +113,93 @@ __global__ void __launch_bounds__(32) residual_final(const double *partials, int
   }
 }
 
+// residual_rows / residual_layers: the same (sum r^2, max |r|) per axis-0
+// LAYER (2D: a row; 3D: a plane) of the owned rows, written to
+// out[layer - own_b][2].  A warp reduces one last-axis row (lane-strided
+// double2 loads, xor-shuffle tree); in 3D a second kernel folds a plane's
+// row partials in a fixed order (one warp per plane).  Every layer's value
+// depends only on the layer's cells, not on how the grid is split across
+// ranks, so the host's exactly rounded sum over layers (math.fsum) gives the
+// same L2 norm on 1 or N GPUs (distributed.srj_solve's residual-L2 rule).
+template <bool VAR, bool NL>
+__global__ void __launch_bounds__(256) residual_rows(const __grid_constant__ ResidParams p,
+                                                     double *rows_out) {
+  const int lane = threadIdx.x & 31;
+  const int ncols = (p.ndim == 2) ? p.n1 : p.n2;
+  const long nrows = (p.ndim == 2) ? long(p.own_e - p.own_b) : long(p.own_e - p.own_b) * p.n1;
+  const long warp0 = (long(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long nwarps = (long(gridDim.x) * blockDim.x) >> 5;
+  for (long row = warp0; row < nrows; row += nwarps) {
+    int64_t base;
+    if (p.ndim == 2) {
+      base = int64_t(p.own_b + int(row)) * p.pitch;
+    } else {
+      const int i = p.own_b + int(row / p.n1), j = int(row % p.n1);
+      base = int64_t(i) * p.plane + int64_t(j) * p.pitch;
+    }
+    double ss = 0.0, mx = 0.0;
+#pragma unroll 4
+    for (int k = lane; k < ncols; k += 32) {
+      const int64_t q = base + k;
+      if (p.act && !p.act[q]) continue;
+      double kk[7];
+      if constexpr (VAR) {
+        for (int a = 0; a < 7; ++a) kk[a] = (a < 1 + 2 * p.ndim) ? p.coef[a][q] : 0.0;
+      } else {
+        for (int a = 0; a < 7; ++a) kk[a] = p.kc[a];
+      }
+      const double *c = p.u + q;
+      const double uc = c[0];
+      const double s = NL ? nl_source(p.f[q], uc) : p.f[q];
+      double r;
+      if (p.ndim == 2)
+        r = resid5(s, kk[0], uc, kk[1], c[-p.pitch], kk[2], c[p.pitch], kk[3], c[-1], kk[4], c[1]);
+      else
+        r = resid7(s, kk[0], uc, kk[1], c[-p.plane], kk[2], c[p.plane], kk[3], c[-p.pitch],
+                   kk[4], c[p.pitch], kk[5], c[-1], kk[6], c[1]);
+      ss = __dadd_rn(ss, __dmul_rn(r, r));
+      acc_max(mx, r);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ss = __dadd_rn(ss, __shfl_xor_sync(kFull, ss, o));
+      const double w = __shfl_xor_sync(kFull, mx, o);
+      mx = (w > mx) ? w : mx;
+    }
+    if (lane == 0) {
+      rows_out[2 * row] = ss;
+      rows_out[2 * row + 1] = mx;
+    }
+  }
+}
+
+// 3D: out[layer] = fixed-order fold of the plane's n1 row partials
+__global__ void __launch_bounds__(256) residual_layers(const double *rows, int nlayers, int n1,
+                                                       double *out) {
+  const int lane = threadIdx.x & 31;
+  const int warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int layer = warp0; layer < nlayers; layer += nwarps) {
+    const double *r = rows + 2 * int64_t(layer) * n1;
+    double ss = 0.0, mx = 0.0;
+    for (int j = lane; j < n1; j += 32) {
+      ss = __dadd_rn(ss, r[2 * j]);
+      const double m = r[2 * j + 1];
+      mx = (m > mx) ? m : mx;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ss = __dadd_rn(ss, __shfl_xor_sync(kFull, ss, o));
+      const double w = __shfl_xor_sync(kFull, mx, o);
+      mx = (w > mx) ? w : mx;
+    }
+    if (lane == 0) {
+      out[2 * layer] = ss;
+      out[2 * layer + 1] = mx;
+    }
+  }
+}
+
 // Ghost-layer refresh after a sweep: GridProblem.refresh_ghosts
 // (grids.py:225-247).  Every face writes only its ghost layer with the other
 // axes restricted to the interior (corners untouched, as the reference) and

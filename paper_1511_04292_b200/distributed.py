@@ -1,33 +1,41 @@
 """Slab (row-block) domain decomposition of the SRJ sweep across GPUs.
 
-The reference has no parallel path (SPEC.md:305 lists distributed memory as a
-non-goal); this module is the multi-GPU design of SURVEY.md section 8(e):
+The reference has no parallel path (``SPEC.md:305`` lists distributed memory
+as a non-goal; the paper only notes that SRJ keeps Jacobi's insensitivity to
+domain decomposition, ``PAPER.md:78-80``).  This module is the multi-GPU
+design of SURVEY.md section 8(e), one process per GPU:
 
-* The global interior is split along axis 0 (slowest, C-order) into contiguous
-  blocks, one per rank (``SlabDecomposition``).
-* Each rank holds its owned rows plus ``halo`` extra rows on every side that
-  has a neighbour.  The local grid treats the layer beyond a halo as a fixed
-  ghost; with ``halo >= fuse`` the stale values there never reach an owned
-  cell within one fused launch of ``fuse`` sweeps (the dependency cone shrinks
-  one row per sweep), so the owned rows are exact.
-* After every fused launch each rank sends its first/last ``halo`` owned rows
-  to its neighbours' halo rows (point-to-point NCCL send/recv of contiguous
-  padded layers -- no packing), which restores the invariant.
-* Per-step (dmax, rmax) are computed over owned rows only and combined with
-  one MAX all-reduce per chunk of steps; MAX is exact, so every rank takes the
-  identical stopping decision and the k-GPU field is bitwise the 1-GPU field.
+* The global interior is split along axis 0 (slowest, C order) into
+  contiguous blocks, one per rank (``SlabDecomposition``).  Each rank holds its
+  owned rows plus ``halo`` >= fuse extra rows on every side with a neighbour,
+  as interior rows of its local plan; the dependency cone of ``fuse`` sweeps
+  shrinks one row per sweep, so the owned rows of a fused launch are exact.
+* ``DeviceSlab`` runs a chunk of steps with ONE C call (``srj_slab_run``): per
+  fused launch, the edge rows the neighbours need are relaxed first, copied
+  into the neighbours' halo rows over NVLink (peer ``cudaMemcpyAsync`` into
+  CUDA-IPC-mapped memory, on a side stream) while the inner rows are relaxed;
+  the ranks order each other on the device with flag words in each other's
+  memory (stream memory operations), so the host only enqueues work.
+* Per-step (dmax, rmax) of owned rows are combined with one MAX all-reduce per
+  chunk (exact), the relative-L2 rule with a SUM all-reduce of per-layer
+  residuals (each layer owned by one rank) and an exactly rounded host sum, so
+  every rank takes the same stopping decision and the N-GPU field, norms and
+  iteration count are bitwise those of the 1-GPU solve (``srj_solve`` below).
 
-The exchange/norm logic is backend-agnostic: ``SlabSolver`` drives any object
-with the ``SlabBackend`` interface.  The product backend is ``DeviceSlab``
-(libsrj kernels on the rank's GPU, NCCL); the CPU tests plug the oracle in
-with the ``gloo`` backend to check the decomposition without GPUs.
+``EmulatedRanks`` drives N slabs on one device through the same C exchange
+(all work enqueued on one stream in dependency order): the 1-GPU test and
+measurement harness of the multi-rank path.
 """
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["DeviceSlab", "SlabDecomposition", "SlabGrid", "SlabSolver"]
+from . import _lib
+
+__all__ = ["DeviceSlab", "DistComm", "EmulatedRanks", "SlabDecomposition", "SlabGrid",
+           "SlabProblem", "jacobi_solve", "srj_solve"]
 
 
 @dataclass(frozen=True)
@@ -85,9 +93,8 @@ class SlabDecomposition:
     def row_parts(self):
         """(edges, inner): owned local interior row ranges [a, b).  ``edges``
         are the rows the neighbours need (sent after every launch), ``inner``
-        the rest (None when the slab is all edge).  The overlapped solver
-        relaxes the edges first, starts the exchange, then relaxes the inner
-        rows while the halo rows travel."""
+        the rest (None when the slab is all edge) -- the split srj_slab_run
+        makes (edges relaxed and sent first, inner rows meanwhile)."""
         lo, hi = self.own_local
         a = lo + (self.halo if self.rank > 0 else 0)
         b = hi - (self.halo if self.rank < self.world - 1 else 0)
@@ -123,229 +130,396 @@ class SlabDecomposition:
         return out
 
 
-class SlabSolver:
-    """Drives a slab backend: fused launches, halo exchange, norm all-reduce.
+def default_halo(ndim, fuse=0):
+    """Fused depth the slab exchanges for: the plan default (2D 4, 3D 2)."""
+    return int(fuse) if fuse else (4 if ndim == 2 else 2)
 
-    backend methods:
-      reserve(nsteps) -- size the per-step norm buffers for a chunk
-      run(src, dst, weights, first, nsteps, norms_offset, rows=None) -- nsteps
-          <= fuse sweeps from buffer src into buffer dst; rows=None relaxes and
-          stores every owned row, rows=(a, b) only local rows [a, b) (the
-          edge / inner split); per-step norms of those rows are folded (MAX)
-          into the chunk's norm buffer at norms_offset
-      layers(buf, first_layer, count) -> contiguous tensor view of layers
-      norms(nsteps) -> tensor [nsteps, 2] (dmax, rmax) of the last chunk
-      comm() -> context manager for the exchange (a side CUDA stream on GPU)
-      comm_fence() -> order the main stream after the exchange (GPU)
 
-    ``overlap`` (default on when the world has neighbours; SRJ_SLAB_OVERLAP=0
-    turns it off): every launch is split into the edge rows the neighbours
-    need and the inner rows; the halo exchange runs on the comm stream
-    concurrently with the inner launch.  Edge and inner rows are
-    disjoint and the exchange touches only edge rows (sent) and halo rows
-    (received) of the destination buffer, so the split changes no value.
-    """
+class SlabProblem:
+    """One rank's rows of a global problem (FIXED faces, constant or per-cell
+    coefficients, linear or nonlinear source) -- built from a global problem
+    every rank holds (``from_global``) or generated rank-locally
+    (``problems.slab_config_fields``), so no rank needs the global field.
 
-    def __init__(self, backend, decomp, group=None, fuse=4, overlap=None):
-        import os
+    ``u``: ghosted local field (local interior rows = owned + halos, plus one
+    layer beyond); ``source`` / ``kappa``, ``center``, ``lower``, ``upper``:
+    local interior-shaped arrays (zero-stride broadcasts for constants)."""
 
-        if fuse > max(1, decomp.halo) and decomp.world > 1:
-            raise ValueError(f"fuse depth {fuse} exceeds halo {decomp.halo}")
-        self.b = backend
-        self.d = decomp
-        self.group = group
-        self.fuse = int(fuse)
-        if overlap is None:
-            overlap = os.environ.get("SRJ_SLAB_OVERLAP", "1") != "0"
-        self.overlap = bool(overlap) and decomp.world > 1
+    def __init__(self, decomp, global_shape, u, center, lower, upper, source=None, kappa=None,
+                 mask=None):
+        self.decomp = decomp
+        self.global_shape = tuple(int(n) for n in global_shape)
+        self.u = u
+        self.source = source if source is not None else np.zeros(np.shape(center))
+        self.kappa = kappa
+        self.center, self.lower, self.upper = center, tuple(lower), tuple(upper)
+        self.mask = mask
+        if self.global_shape[0] != decomp.n0:
+            raise ValueError("decomposition does not match the global shape")
+        a, b = decomp.local_rows
+        if tuple(np.shape(center)) != (b - a,) + self.global_shape[1:]:
+            raise ValueError("local arrays do not match the decomposition")
 
-    def _post_exchange(self, buf):
-        import torch.distributed as dist
+    @property
+    def ndim(self):
+        return len(self.global_shape)
 
-        ops = []
-        for peer, first, count in self.d.recvs():
-            ops.append(dist.P2POp(dist.irecv, self.b.layers(buf, first, count), peer,
-                                  group=self.group))
-        for peer, first, count in self.d.sends():
-            ops.append(dist.P2POp(dist.isend, self.b.layers(buf, first, count), peer,
-                                  group=self.group))
-        return dist.batch_isend_irecv(ops)
+    @classmethod
+    def from_global(cls, problem, decomp):
+        """Slice a GridProblem-like object (FIXED faces, no post_sweep hook)."""
+        for pair in getattr(problem, "bc", ()):
+            for rule in pair:
+                if rule.kind != "fixed":
+                    raise NotImplementedError("the slab decomposition supports FIXED faces only")
+        if getattr(problem, "post_sweep", None) is not None:
+            raise NotImplementedError("post_sweep hooks need the whole grid on one GPU")
+        shape = problem.source.shape
+        sl = decomp.local_interior
+        br = lambda a: sl(np.broadcast_to(a, shape))  # noqa: E731
+        kappa = getattr(problem, "source_kappa", None)
+        mask = getattr(problem, "mask", None)
+        return cls(decomp, shape, decomp.local_field(problem.u), br(problem.center),
+                   tuple(br(a) for a in problem.lower), tuple(br(a) for a in problem.upper),
+                   source=sl(problem.source), kappa=None if kappa is None else sl(kappa),
+                   mask=None if mask is None else sl(mask))
 
-    def exchange(self, buf):
-        if self.d.world == 1:
-            return
-        for req in self._post_exchange(buf):
-            req.wait()
+    def owned_source_sq(self):
+        """Per owned layer sum of squares of the source (L2 rule reference)."""
+        from .grids import layer_sum_squares
 
-    def run(self, src, weights, first, nsteps):
-        """Steps [first, first+nsteps) from buffer ``src``; returns (dst, norms).
+        lo, hi = self.decomp.own_local
+        return layer_sum_squares(np.asarray(self.source)[lo:hi])
 
-        ``src`` is left untouched (chunk snapshot); the result lands in one of
-        the two other buffers.  ``norms`` is a host array [nsteps, 2] already
-        reduced over ranks.
-        """
+
+class DistComm:
+    """MAX / SUM all-reduces of host arrays over a torch.distributed group
+    (NCCL: staged through the rank's GPU; gloo: on the host)."""
+
+    def __init__(self, group=None, device=None):
         import torch
         import torch.distributed as dist
 
-        self.b.reserve(nsteps)
-        others = [i for i in range(3) if i != src]
-        cur, k, flip = src, 0, 0
-        edges, inner = self.d.row_parts() if self.overlap else (None, None)
-        while k < nsteps:
-            t = min(self.fuse, nsteps - k)
-            dst = others[flip]
-            if not self.overlap:
-                self.b.run(cur, dst, weights, first + k, t, k)
-                self.exchange(dst)
-            else:
-                for rows in edges:
-                    self.b.run(cur, dst, weights, first + k, t, k, rows=rows)
-                with self.b.comm():
-                    reqs = self._post_exchange(dst)
-                if inner is not None:
-                    self.b.run(cur, dst, weights, first + k, t, k, rows=inner)
-                with self.b.comm():
-                    for req in reqs:
-                        req.wait()
-                self.b.comm_fence()
-            cur, flip, k = dst, 1 - flip, k + t
-        norms = self.b.norms(nsteps)
-        if self.d.world > 1:
-            dist.all_reduce(norms, op=dist.ReduceOp.MAX, group=self.group)
-        if isinstance(norms, torch.Tensor):
-            norms = norms.cpu().numpy()
-        return cur, np.asarray(norms).reshape(nsteps, 2)
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        nccl = dist.get_backend(group) == "nccl"
+        self.device = (device if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())) if nccl else torch.device("cpu")
+        self.torch = torch
+
+    def _reduce(self, a, op):
+        t = self.torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(self.device)
+        self.dist.all_reduce(t, op=op, group=self.group)
+        return t.cpu().numpy()
+
+    def max_(self, a):
+        return self._reduce(a, self.dist.ReduceOp.MAX)
+
+    def sum_(self, a):
+        return self._reduce(a, self.dist.ReduceOp.SUM)
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+    def all_gather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
 
 
 class DeviceSlab:
-    """GPU backend: this rank's rows in a ``DeviceGrid`` (libsrj kernels)."""
+    """One rank's slab on its GPU: a pooled ``DeviceGrid`` (three fields +
+    flag words in one allocation) and the C slab exchange (``srj_slab_*``)."""
 
-    def __init__(self, fields, decomp, device=None):
+    def __init__(self, slab, device=None):
         from .engine import DeviceGrid
 
-        d = decomp
-        kappa = fields.get("kappa")
-        sl = d.local_interior
-        self.grid = DeviceGrid(
-            d.local_field(fields["u"]), sl(fields["source"]), sl(fields["center"]),
-            tuple(sl(a) for a in fields["lower"]), tuple(sl(a) for a in fields["upper"]),
-            active=None if fields.get("mask") is None else sl(fields["mask"]),
-            kappa=None if kappa is None else sl(kappa), own=d.own_local, device=device)
-        self.plane = int(self.grid.layout.plane)
-        self.origin = int(self.grid.layout.origin)
-        self.stream = self.grid.stream
-        # deepest single-launch fusion the plan runs (libsrj srj_plan_run)
-        self.max_fuse = (4 if self.grid.ndim == 2 else 3) if self.grid.constant else 1
-        self._part_norms = None
-        self._comm = None
-        edges, _ = decomp.row_parts()
-        # the overlapped solver runs the edges first (a single rank has none)
-        self._first_part = edges[0] if edges else None
-
-    def reserve(self, nsteps):
-        torch = self.grid.torch
-        self.grid.ensure_norms(nsteps)
-        if self._part_norms is None or self._part_norms.numel() < 2 * nsteps:
-            self._part_norms = torch.zeros(2 * max(nsteps, 1), dtype=torch.float64,
-                                           device=self.grid.device)
-
-    def run(self, src, dst, weights, first, nsteps, norms_offset, rows=None):
+        d = slab.decomp
+        self.decomp = d
+        self.problem = slab
+        self.grid = DeviceGrid(slab.u, slab.source, slab.center, slab.lower, slab.upper,
+                               active=slab.mask, kappa=slab.kappa, own=d.own_local,
+                               device=device, pooled=True)
         g = self.grid
-        if rows is None:
-            g.run_single(g.plan, src, dst, weights, first, nsteps,
-                         g.norms[2 * norms_offset:])
-            return
-        # edge / inner launch: its own plan over the same fields; per-step
-        # norms folded into the chunk buffer (the first part of a launch
-        # overwrites, later ones take the MAX -- exact, order-free)
-        part = self._part_norms[:2 * nsteps]
-        g.run_single(g.sub_plan(*rows), src, dst, weights, first, nsteps, part)
-        with g._on(), g.torch.cuda.stream(g.stream):
-            view = g.norms[2 * norms_offset:2 * (norms_offset + nsteps)]
-            if rows == self._first_part:
-                view.copy_(part)
-            else:
-                g.torch.maximum(view, part, out=view)
+        self.lib = g.lib
+        self.stream = g.stream
+        self.n_layers = d.n0
+        self.layer0 = d.owned[0]
+        self._opened = []
+        bufs = (ctypes.c_void_p * 3)(*[f.data_ptr() for f in g.fields])
+        self.handle = ctypes.c_void_p()
+        with g._on():
+            _lib.check(self.lib.srj_slab_create(
+                ctypes.byref(g.desc), int(d.halo), bufs, ctypes.c_void_p(g.flags.data_ptr()),
+                int(d.rank > 0), int(d.rank < d.world - 1), ctypes.byref(self.handle)),
+                "srj_slab_create")
+        self._peer_ptrs = None
 
-    def comm(self):
-        """Exchange context: the comm stream, ordered after the work queued
-        so far on the main stream (the edge launches)."""
-        import contextlib
+    # ---------------------------------------------------------------- wiring
+    def _peer_struct(self, bufs, flags, dst_row):
+        p = _lib.SrjSlabPeer()
+        for i in range(3):
+            p.bufs[i] = bufs[i]
+        p.flags = flags
+        p.dst_row = int(dst_row)
+        return p
 
+    def connect_local(self, lower=None, upper=None):
+        """Neighbours in the same process on the same device (emulated ranks)."""
+        for side, nb in ((0, lower), (1, upper)):
+            if nb is None:
+                continue
+            dst_row = nb.decomp.own_local[1] if side == 0 else 0
+            p = self._peer_struct([f.data_ptr() for f in nb.grid.fields],
+                                  nb.grid.flags.data_ptr(), dst_row)
+            _lib.check(self.lib.srj_slab_connect(self.handle, side, ctypes.byref(p)),
+                       "srj_slab_connect")
+
+    def connect(self, comm):
+        """Map the neighbours' pooled buffers through CUDA IPC (one process per
+        GPU) and wire the exchange; then reset the flags on every rank."""
         g = self.grid
-        torch = g.torch
-        if self._comm is None:
-            self._comm = torch.cuda.Stream(device=g.device)
-        self._comm.wait_stream(g.stream)
-        stack = contextlib.ExitStack()
-        stack.enter_context(g._on())
-        stack.enter_context(torch.cuda.stream(self._comm))
-        return stack
+        h = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64()
+        with g._on():
+            _lib.check(self.lib.srj_ipc_get_handle(ctypes.c_void_p(g.pool.data_ptr()), h,
+                                                   ctypes.byref(off)), "srj_ipc_get_handle")
+        elems = int(g.layout.elems)
+        info = {"handle": h.raw, "offset": off.value, "elems": elems,
+                "own_e": self.decomp.own_local[1], "rank": self.decomp.rank}
+        infos = comm.all_gather_object(info)
+        r = self.decomp.rank
+        for side, peer in ((0, r - 1), (1, r + 1)):
+            if not 0 <= peer < self.decomp.world:
+                continue
+            pi = infos[peer]
+            ptr = ctypes.c_void_p()
+            with g._on():
+                _lib.check(self.lib.srj_ipc_open(pi["handle"], int(pi["offset"]),
+                                                 ctypes.byref(ptr)), "srj_ipc_open")
+            self._opened.append(int(ptr.value) - int(pi["offset"]))
+            base = int(ptr.value)
+            bufs = [base + 8 * i * pi["elems"] for i in range(3)]
+            flags = base + 8 * 3 * pi["elems"]
+            dst_row = pi["own_e"] if side == 0 else 0
+            p = self._peer_struct(bufs, flags, dst_row)
+            _lib.check(self.lib.srj_slab_connect(self.handle, side, ctypes.byref(p)),
+                       "srj_slab_connect")
+        self.reset()
+        comm.barrier()
 
-    def comm_fence(self):
-        """The next launch reads the received halo rows: main waits comm."""
-        self.grid.stream.wait_stream(self._comm)
+    def reset(self):
+        g = self.grid
+        with g._on():
+            _lib.check(self.lib.srj_slab_reset(self.handle, g._sp), "srj_slab_reset")
+        g.stream.synchronize()
 
-    def layers(self, buf, first, count):
-        f = self.grid.fields[buf]
-        return f[first * self.plane:(first + count) * self.plane]
+    # --------------------------------------------------------------- running
+    def run_chunk(self, src, weights, first, n, fuse=0):
+        return run_slabs([self], src, weights, first, n, fuse)
 
-    def norms(self, nsteps):
-        return self.grid.norms[:2 * nsteps].clone()
+    def norms(self, n):
+        return self.grid.norms[:2 * n].view(n, 2).cpu().numpy()
 
-    @property
-    def owned_cells(self):
-        lo, hi = self.grid.desc.own0_begin, self.grid.desc.own0_end
-        return int(hi - lo) * int(np.prod(self.grid.shape[1:]))
+    def residual_layers(self, buf):
+        return self.grid.residual_layers(buf)
 
     def download_owned(self, buf):
         """Owned rows of buffer ``buf`` as a host array (interior columns)."""
-        lay = self.grid.layout
         u = np.empty(tuple(int(x) + 2 for x in self.grid.shape))
         self.grid.download_field(buf, u)
-        lo, hi = self.grid.desc.own0_begin, self.grid.desc.own0_end
+        lo, hi = self.decomp.own_local
         inner = (slice(1, -1),) * (u.ndim - 1)
         return u[(slice(1 + lo, 1 + hi),) + inner]
 
+    @property
+    def owned_cells(self):
+        lo, hi = self.decomp.own_local
+        return int(hi - lo) * int(np.prod(self.grid.shape[1:]))
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            with self.grid._on():
+                self.lib.srj_slab_destroy(self.handle)
+                for base in self._opened:
+                    self.lib.srj_ipc_close(ctypes.c_void_p(base))
+            self.handle = None
+            self._opened = []
+        self.grid.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_slabs(slabs, src, weights, first, n, fuse=0):
+    """One srj_slab_run over ``slabs`` (1 = this process's rank; more = ranks
+    emulated on one device, enqueued on the first slab's stream)."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    k = len(slabs)
+    for s in slabs:
+        s.grid.ensure_norms(max(n, 1))
+    handles = (ctypes.c_void_p * k)(*[s.handle.value for s in slabs])
+    norms = (ctypes.c_void_p * k)(*[s.grid.norms.data_ptr() for s in slabs])
+    streams = (ctypes.c_void_p * k)(*[s.stream.cuda_stream for s in slabs])
+    out = ctypes.c_int32(0)
+    with slabs[0].grid._on():
+        _lib.check(slabs[0].lib.srj_slab_run(
+            handles, k, int(src), w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(w),
+            int(first), int(n), int(fuse), norms, ctypes.byref(out), streams), "srj_slab_run")
+    return int(out.value)
+
+
+class EmulatedRanks:
+    """``world`` ranks of a slab decomposition on ONE device in one process,
+    exchanging through the same C path (``srj_slab_run`` with all slabs, one
+    stream); the backend interface of ``solver.run_solve`` with the rank
+    combination done here (use ``solver.LocalComm``)."""
+
+    def __init__(self, problem, world, fuse=0, device=None):
+        nd = problem.source.ndim
+        halo = default_halo(nd, fuse)
+        n0 = problem.source.shape[0]
+        self.decomps = [SlabDecomposition(n0, world, r, halo) for r in range(world)]
+        self.slabs = [DeviceSlab(SlabProblem.from_global(problem, d), device) for d in self.decomps]
+        for r, s in enumerate(self.slabs):
+            s.connect_local(self.slabs[r - 1] if r > 0 else None,
+                            self.slabs[r + 1] if r + 1 < world else None)
+        for s in self.slabs:
+            s.reset()
+        self.n_layers = n0
+        self.layer0 = 0
+        self.stream = self.slabs[0].stream
+
+    def run_chunk(self, src, weights, first, n, fuse=0):
+        return run_slabs(self.slabs, src, weights, first, n, fuse)
+
+    def norms(self, n):
+        return np.max([s.norms(n) for s in self.slabs], axis=0)
+
+    def residual_layers(self, buf):
+        return np.concatenate([s.residual_layers(buf) for s in self.slabs])
+
+    def download_owned(self, buf):
+        return np.concatenate([s.download_owned(buf) for s in self.slabs])
+
+    def close(self):
+        for s in self.slabs:
+            s.close()
+
+
+def _comm_for(group):
+    import torch.distributed as dist
+
+    from .solver import LocalComm
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        return DistComm(group)
+    return LocalComm
+
+
+def _solve(problem, weights, tol, max_iters, normalise, stop, check_every, fuse, chunk,
+           l2_reference, group, gather, device):
+    from . import grids as G
+    from .solver import l2_from_layers, run_solve, source_l2
+
+    comm = _comm_for(group)
+    if isinstance(problem, SlabProblem):
+        slab = problem
+        if slab.decomp.world != comm.world or slab.decomp.rank != comm.rank:
+            raise ValueError("SlabProblem decomposition does not match the process group")
+    else:
+        nd = problem.source.ndim
+        d = SlabDecomposition(problem.source.shape[0], comm.world, comm.rank,
+                              default_halo(nd, fuse))
+        slab = SlabProblem.from_global(problem, d)
+    backend = DeviceSlab(slab, device)
+    try:
+        if comm.world > 1:
+            backend.connect(comm)
+        else:
+            backend.reset()
+        if stop == "residual_l2" and l2_reference is None:
+            if slab.kappa is not None:
+                l2_reference = lambda: l2_from_layers(  # noqa: E731 - residual of u0
+                    backend, comm, backend.residual_layers(0))[0]
+            else:
+                l2_reference = source_l2(backend, comm, slab.owned_source_sq())
+        hist, converged, diverged, cur = run_solve(
+            backend, comm, weights, tol, max_iters, normalise, stop, check_every, fuse, chunk,
+            l2_reference, int(np.prod(slab.global_shape)))
+        owned = backend.download_owned(cur)
+    finally:
+        backend.close()
+    out = G._history(hist, float(tol), converged)
+    if gather and not isinstance(problem, SlabProblem):
+        parts = comm.all_gather_object(owned) if comm.world > 1 else [owned]
+        inner = (slice(1, -1),) * (problem.u.ndim - 1)
+        problem.u[(slice(1, 1 + problem.source.shape[0]),) + inner] = np.concatenate(parts)
+    G._raise_if_diverged(out, diverged)
+    return out, owned
+
+
+def srj_solve(problem, cycle, tol, max_iters=10_000_000, *, group=None, stop="update_inf",
+              check_every=None, fuse=0, chunk=None, l2_reference=None, gather=False,
+              device=None):
+    """``grids.srj_solve`` (reference ``grids.py:642-687``) over the ranks of
+    a process group, one GPU per rank.
+
+    ``problem``: a global GridProblem (FIXED faces) that every rank holds, or
+    this rank's ``SlabProblem``.  Returns (history, owned interior rows of this
+    rank); ``gather=True`` also writes the whole interior into ``problem.u`` on
+    every rank.  History, iteration count and field are bitwise those of the
+    single-GPU ``grids.srj_solve`` under both stopping rules; a
+    ``DivergenceError`` is raised on every rank at the same step."""
+    return _solve(problem, cycle.weight_sequence, tol, max_iters, True, stop, check_every, fuse,
+                  chunk, l2_reference, group, gather, device)
+
+
+def jacobi_solve(problem, tol, max_iters=10_000_000, *, group=None, stop="update_inf",
+                 check_every=None, fuse=0, chunk=None, l2_reference=None, gather=False,
+                 device=None):
+    """``grids.jacobi_solve`` (``grids.py:690-694``, omega = 1) over ranks."""
+    return _solve(problem, np.ones(1), tol, max_iters, False, stop, check_every, fuse, chunk,
+                  l2_reference, group, gather, device)
+
 
 class SlabGrid:
-    """Benchmark/solver facade: one rank's slab with the DeviceGrid-like API
-    (``run``, ``norms``, ``stream``) used by bench.py."""
+    """Benchmark facade: this rank's slab with the DeviceGrid-like API
+    (``run``, ``norms``, ``stream``) used by bench.py; per-step norms are
+    MAX-reduced over the group once per ``run``."""
 
-    def __init__(self, fields, rank, world, fuse=4, group=None):
-        import torch
+    def __init__(self, slab, comm=None, device=None):
+        from .solver import LocalComm
 
-        n0 = fields["source"].shape[0]
-        self.fields = fields  # the global problem (host); the e2e bench re-uploads from it
-        self.decomp = SlabDecomposition(n0, world, rank, halo=max(1, fuse))
-        self.backend = DeviceSlab(fields, self.decomp)
-        fuse = max(1, min(fuse, self.backend.max_fuse))
-        self.solver = SlabSolver(self.backend, self.decomp, group=group, fuse=fuse)
+        self.comm = comm or LocalComm
+        self.decomp = slab.decomp
+        self.problem = slab
+        self.backend = DeviceSlab(slab, device)
+        if self.comm.world > 1:
+            self.backend.connect(self.comm)
+        else:
+            self.backend.reset()
         self.stream = self.backend.stream
         self._norms = None
-        self.torch = torch
-
-    @classmethod
-    def weak_rows(cls, base, rank, world, fuse=4):
-        """cfg2 weak scaling: stack ``world`` copies of the per-GPU row count
-        into a (rows*world) x cols grid built with the same recipe."""
-        from .problems import CONFIGS, poisson_fields
-
-        n0, n1 = base["source"].shape
-        cfg = CONFIGS["cfg2"]
-        fields = poisson_fields((n0 * world, n1), cfg["n_gauss"], cfg["seed"], cfg["noise"],
-                                cfg["width"])
-        return cls(fields, rank, world, fuse=fuse)
 
     @property
     def owned_cells(self):
         return self.backend.owned_cells
 
     def run(self, cur, weights, first, nsteps, fuse=0):
-        dst, norms = self.solver.run(cur, weights, first, nsteps)
-        self._norms = norms
+        dst = self.backend.run_chunk(cur, weights, first, nsteps, fuse)
+        self._norms = self.comm.max_(self.backend.norms(nsteps))
         return dst
 
     @property
     def norms(self):
-        return self.torch.from_numpy(np.ascontiguousarray(self._norms).reshape(-1))
+        import torch
+
+        return torch.from_numpy(np.ascontiguousarray(self._norms).reshape(-1))
+
+    def close(self):
+        self.backend.close()

@@ -65,7 +65,7 @@ class DeviceGrid:
 
     def __init__(self, u, source, center, lower, upper, active=None, kappa=None,
                  halo0=1, own=None, physical=(True, True), device=None, bc=None,
-                 post_gather=None):
+                 post_gather=None, pooled=False):
         torch = require_cuda()
         lib = _lib.load()
         self.torch = torch
@@ -86,8 +86,17 @@ class DeviceGrid:
         with torch.cuda.device(self.device):
             self.stream = torch.cuda.current_stream(self.device)
             self._keep = []
-            self.fields = [torch.zeros(elems, dtype=torch.float64, device=self.device)
-                           for _ in range(3)]
+            if pooled:
+                # one allocation for the three fields + the slab exchange's
+                # flag words, so a single CUDA IPC handle maps all of them
+                # into the neighbour ranks (distributed.DeviceSlab)
+                self.pool = torch.zeros(3 * elems + 16, dtype=torch.float64, device=self.device)
+                self.fields = [self.pool[i * elems:(i + 1) * elems] for i in range(3)]
+                self.flags = self.pool[3 * elems:3 * elems + 16].view(torch.int32)
+            else:
+                self.pool = None
+                self.fields = [torch.zeros(elems, dtype=torch.float64, device=self.device)
+                               for _ in range(3)]
             # one host->device copy; the other two buffers (whose ghost layers
             # the kernels never write) are device copies of it
             self.upload_field(_contig(u, np.float64), self.fields[0])
@@ -302,6 +311,20 @@ class DeviceGrid:
                 ctypes.c_void_p(self.resid_out.data_ptr()), self._sp), "srj_plan_residual")
         v = self.resid_out.cpu().numpy()
         return float(v[0]), float(v[1])
+
+    def residual_layers(self, idx):
+        """Per owned axis-0 layer (sum r^2, max|r|) of field buffer ``idx``
+        as a host array [layers, 2] (srj_plan_residual_layers; synchronous)."""
+        lo, hi = int(self.desc.own0_begin), int(self.desc.own0_end)
+        n = max(hi - lo, 0)
+        if getattr(self, "_layers", None) is None or self._layers.numel() < 2 * max(n, 1):
+            self._layers = self.torch.zeros(2 * max(n, 1), dtype=self.torch.float64,
+                                            device=self.device)
+        with self._on():
+            _lib.check(self.lib.srj_plan_residual_layers(
+                self.plan, ctypes.c_void_p(self.fields[idx].data_ptr()),
+                ctypes.c_void_p(self._layers.data_ptr()), self._sp), "srj_plan_residual_layers")
+        return self._layers[:2 * n].view(n, 2).cpu().numpy()
 
     def close(self):
         subs = self.__dict__.pop("_sub_plans", {})

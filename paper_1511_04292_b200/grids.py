@@ -39,7 +39,6 @@ M-cycle) with the fused residual kernel; it is an addition, not in the
 reference.
 """
 
-import math
 import time
 from dataclasses import dataclass, field
 
@@ -353,8 +352,34 @@ def weighted_jacobi_sweep(problem, omega, traversal="forward"):
     return float(norms[0]), float(norms[1])
 
 
-def _solve(problem, weights, tol, max_iters, normalise, stop, check_every, fuse,
-           chunk, l2_reference):
+def layer_sum_squares(a):
+    """Per axis-0 layer sum of squares (numpy pairwise, a function of the
+    layer's values only): the L2 rule's reference norm ||source||_2 is the
+    exactly rounded sum of these (``solver.source_l2``)."""
+    a = np.asarray(a, dtype=np.float64)
+    return np.sum(np.square(a), axis=tuple(range(1, a.ndim)))
+
+
+def _history(hist, tol, converged):
+    return ResidualHistory(residual_inf=hist["residual_inf"],
+                           true_residual_inf=hist["true_residual_inf"],
+                           seconds=hist["seconds"], tolerance=tol, converged=converged,
+                           relative_l2=hist["relative_l2"])
+
+
+def _raise_if_diverged(hist, diverged):
+    if diverged:
+        hist.converged = False
+        dmax = float(hist.residual_inf[-1])
+        raise DivergenceError(
+            f"update norm {dmax:.3e} exceeds the overflow guard after "
+            f"{hist.iterations} steps", hist.iterations, hist)
+
+
+def _solve(problem, weights, tol, max_iters, normalise, stop, check_every, fuse, chunk,
+           l2_reference):
+    from .solver import GridBackend, LocalComm, l2_from_layers, run_solve, source_l2
+
     tol = float(tol)
     if tol <= 0.0:
         raise ValueError("tolerance must be positive")
@@ -362,87 +387,24 @@ def _solve(problem, weights, tol, max_iters, normalise, stop, check_every, fuse,
         raise ValueError("max_iters must be at least 1")
     if stop not in ("update_inf", "residual_l2"):
         raise ValueError(f"unknown stopping rule {stop!r}")
-    w = np.asarray(weights, dtype=np.float64)
-    m = len(w)
-    absw = np.abs(w) if normalise else np.ones(m)
     dev = _device_grid(problem)
-    start = time.perf_counter()
-    diffs, resids, secs, l2s = [], [], [], []
-    converged = False
-    diverged_at = None
-    cur = 0
-    done = 0
-    if stop == "residual_l2":
-        every = int(check_every or m)
-        if every < 1:
-            raise ValueError("check_every must be at least 1")
-        if l2_reference is None:
-            if getattr(problem, "source_kappa", None) is not None:
-                l2_reference = math.sqrt(dev.residual(cur)[0])
-            else:
-                l2_reference = float(np.sqrt(np.sum(np.square(problem.source))))
-        if l2_reference == 0.0:
-            l2_reference = 1.0
-        span = cap = every
-    elif chunk:
-        span = cap = int(chunk)
-    else:
-        # host checks of the per-step norms: the first chunk covers ~2 ms of
-        # work, each next one doubles up to ~50 ms, so replaying the chunk in
-        # which the rule fires costs at most about as much as the work so far
-        est = _step_seconds_estimate(problem)
-        cap = int(min(65536, max(64, 0.05 / est)))
-        span = int(min(cap, max(32, 0.002 / est)))
     try:
-        while done < max_iters:
-            n = min(span, max_iters - done)
-            span = min(cap, 2 * span)
-            if stop == "residual_l2":
-                n = min(n, every - done % every)
-            out = dev.run(cur, w, done, n, fuse)
-            norms = dev.norms[:2 * n].view(n, 2).cpu().numpy()
-            t_now = time.perf_counter() - start
-            t_prev = float(secs[-1][-1]) if secs else 0.0
-            metric = norms[:, 0] / absw[(done + np.arange(n)) % m]
-            bad = ~np.isfinite(metric) | (metric > OVERFLOW_LIMIT)
-            hit = metric < tol if stop == "update_inf" else np.zeros(n, dtype=bool)
-            events = np.flatnonzero(bad | hit)
-            take = n if events.size == 0 else int(events[0]) + 1
-            if take < n:
-                out = dev.run(cur, w, done, take, fuse)  # replay to the exact step
-            diffs.append(metric[:take])
-            resids.append(norms[:take, 1])
-            secs.append(t_prev + (t_now - t_prev) * np.arange(1, take + 1) / take)
-            done += take
-            cur = out
-            if events.size:
-                if bad[take - 1]:
-                    diverged_at = take - 1
-                else:
-                    converged = True
-                break
-            if stop == "residual_l2" and done % every == 0:
-                rel = math.sqrt(dev.residual(cur)[0]) / l2_reference
-                l2s.append((done, rel))
-                if rel < tol:
-                    converged = True
-                    break
+        backend = GridBackend(dev, problem.source.shape[0])
+        if stop == "residual_l2" and l2_reference is None:
+            if getattr(problem, "source_kappa", None) is not None:
+                l2_reference = lambda: l2_from_layers(  # noqa: E731 - residual of u0
+                    backend, LocalComm, dev.residual_layers(0))[0]
+            else:
+                l2_reference = source_l2(backend, LocalComm, layer_sum_squares(problem.source))
+        hist, converged, diverged, cur = run_solve(
+            backend, LocalComm, weights, tol, max_iters, normalise, stop, check_every, fuse,
+            chunk, l2_reference, int(np.prod(problem.source.shape)))
         dev.download_field(cur, problem.u)  # ghosts refreshed on the device
     finally:
         dev.close()
-    hist = ResidualHistory(
-        residual_inf=np.concatenate(diffs) if diffs else np.zeros(0),
-        true_residual_inf=np.concatenate(resids) if resids else np.zeros(0),
-        seconds=np.concatenate(secs) if secs else np.zeros(0),
-        tolerance=tol, converged=converged,
-        relative_l2=np.asarray(l2s, dtype=float).reshape(-1, 2))
-    if diverged_at is not None:
-        hist.converged = False
-        dmax = float(hist.residual_inf[-1])
-        raise DivergenceError(
-            f"update norm {dmax:.3e} exceeds the overflow guard after "
-            f"{hist.iterations} steps", hist.iterations, hist)
-    return hist, problem.interior
+    out = _history(hist, tol, converged)
+    _raise_if_diverged(out, diverged)
+    return out, problem.interior
 
 
 def srj_solve(problem, cycle, tol, max_iters=10_000_000, *, stop="update_inf",

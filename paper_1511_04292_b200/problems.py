@@ -25,7 +25,7 @@ import math
 import numpy as np
 
 __all__ = ["CONFIGS", "gaussian_sum", "poisson_fields", "nonlinear_fields",
-           "config_fields", "config_schedule"]
+           "config_fields", "config_schedule", "slab_config_fields"]
 
 # BASELINE.json configs -> (shape, P, table-N, source recipe)
 CONFIGS = {
@@ -72,15 +72,20 @@ def config_schedule(name, table=None, optimal=False):
     return quantize(table.lookup(cfg["p"], int(n)))
 
 
-def _axes(shape):
-    return [np.arange(1, n + 1, dtype=np.float64) / (n + 1) for n in shape]
+def _axes(shape, rows=None):
+    """Node coordinates per axis; ``rows=(a, b)`` keeps axis-0 rows [a, b)."""
+    axes = [np.arange(1, n + 1, dtype=np.float64) / (n + 1) for n in shape]
+    if rows is not None:
+        axes[0] = axes[0][rows[0]:rows[1]]
+    return axes
 
 
-def gaussian_sum(shape, rng, n_gauss, width, amp=(-1.0, 1.0), peak=None):
-    """Sum of seeded Gaussians on the vertex-centred interior grid."""
+def gaussian_sum(shape, rng, n_gauss, width, amp=(-1.0, 1.0), peak=None, rows=None):
+    """Sum of seeded Gaussians on the vertex-centred interior grid (only
+    axis-0 rows [a, b) when ``rows`` is given: same draws, same values)."""
     nd = len(shape)
-    axes = _axes(shape)
-    out = np.zeros(shape)
+    axes = _axes(shape, rows)
+    out = np.zeros(tuple(len(x) for x in axes))
     for _ in range(n_gauss):
         centre = rng.uniform(0.1, 0.9, nd)
         w = rng.uniform(*width)
@@ -212,6 +217,46 @@ def grad_shafranov_fields(test, c, n):
     return {"u": u, "source": np.zeros(shape), "center": center, "lower": (rad, th_lo),
             "upper": (rad.copy(), th_hi), "mask": mask,
             "bc": (("fixed", "fixed"), ("mirror", "mirror"))}
+
+
+def _noise_rows(rng, shape, rows):
+    """Rows [a, b) of ``rng.uniform(-1, 1, shape)`` without drawing the rest:
+    every double is one 64-bit PCG64 output, so the generator is advanced past
+    the a * (cells per row) draws of the rows before (rank-local inputs,
+    tested against the global draw)."""
+    per_row = int(np.prod(shape[1:]))
+    bitgen = rng.bit_generator
+    bitgen.advance(rows[0] * per_row)
+    return rng.uniform(-1.0, 1.0, (rows[1] - rows[0],) + tuple(shape[1:]))
+
+
+def slab_config_fields(name, decomp, shape=None):
+    """Rank-local inputs of a BASELINE config for a ``SlabDecomposition``:
+    the rows [a, b) = ``decomp.local_rows`` (owned + halos) of what
+    ``config_fields`` builds, computed without the global arrays (Gaussians
+    evaluated on the local rows, noise drawn with a PCG64 ``advance``), so a
+    32768^2 grid costs each rank only its slab.  Returns a
+    ``distributed.SlabProblem``."""
+    from .distributed import SlabProblem
+
+    cfg = CONFIGS[name]
+    shape = tuple(int(n) for n in (shape or cfg["shape"]))
+    a, b = decomp.local_rows
+    local = (b - a,) + shape[1:]
+    rng = np.random.default_rng(cfg["seed"])
+    center, lower, upper = _stencil(shape)
+    bc = lambda x: np.broadcast_to(x.reshape(-1)[:1].reshape(()), local)  # noqa: E731
+    center, lower, upper = bc(center), tuple(bc(x) for x in lower), tuple(bc(x) for x in upper)
+    # ghosted local field: rows [a-1, b+1) of the global ghosted field
+    ug = tuple(n + 2 for n in local)
+    if cfg.get("nonlinear"):
+        rho = gaussian_sum(shape, rng, 4, width=(0.05, 0.15), peak=(0.01, 0.1), rows=(a, b))
+        return SlabProblem(decomp, shape, np.ones(ug), center, lower, upper,
+                           source=np.zeros(local), kappa=(2.0 * math.pi) * rho)
+    f = gaussian_sum(shape, rng, cfg["n_gauss"], cfg["width"], rows=(a, b))
+    if cfg["noise"]:
+        f += _noise_rows(rng, shape, (a, b))
+    return SlabProblem(decomp, shape, np.zeros(ug), center, lower, upper, source=-f)
 
 
 def config_fields(name, shape=None):
