@@ -73,10 +73,11 @@ def test_cfg3_full_size_first_64_sweeps():
 
 def test_cfg5_relative_l2_solve_iteration_count():
     """cfg5's stopping rule (relative L2 1e-8 of the initial residual, checked
-    every M-cycle) on a 64^3 grid of the cfg5 recipe: the same iteration
+    every M-cycle) on a 128^3 grid of the cfg5 recipe (on 64^3 the N=150 row over-relaxes
+    the psi^5 feedback and diverges in both): the same iteration
     count and check values as the oracle's solve, and the same field."""
     cyc = config_schedule("cfg5")
-    f = config_fields("cfg5", (64, 64, 64))
+    f = config_fields("cfg5", (128, 128, 128))
     want = problem_from(f)
     steps, status, _, checks = oracle.solve(want, cyc.weight_sequence, 1e-8, max_iters=200 * cyc.m,
                                             rule="residual_l2", kappa=f["kappa"],
@@ -102,3 +103,20 @@ def test_cfg2_relative_l2_solve_iteration_count_reduced():
     assert hist.iterations == steps and hist.converged == (status == 1)
     assert np.array_equal(p.u, want.u)
     np.testing.assert_allclose(hist.relative_l2[:, 1], [c[1] for c in checks], rtol=1e-12)
+
+
+def test_cfg5_schedule_divergence_on_small_grid_same_step():
+    """On 64^3 the cfg5 schedule over-relaxes the psi^5 feedback: the GPU
+    solve raises DivergenceError at the same step the oracle's overflow guard
+    fires (grids.py:618-625), with the same history."""
+    cyc = config_schedule("cfg5")
+    f = config_fields("cfg5", (64, 64, 64))
+    want = problem_from(f)
+    steps, status, norms, _ = oracle.solve(want, cyc.weight_sequence, 1e-8, max_iters=200 * cyc.m,
+                                           rule="residual_l2", kappa=f["kappa"], nthreads=THREADS)
+    assert status == 2
+    p = problem_from(f)
+    with pytest.raises(G.DivergenceError) as exc:
+        G.srj_solve(p, cyc, 1e-8, max_iters=200 * cyc.m, stop="residual_l2")
+    assert exc.value.iterations == steps
+    assert np.array_equal(exc.value.history.true_residual_inf, norms[:, 1])

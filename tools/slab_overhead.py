@@ -10,7 +10,7 @@ DESIGN.md target is < 10%.  Also reports the device time per fused step of
 the emulated 8-rank run vs the 1-rank plan (the cost of the edge/inner split
 on one GPU; on real GPUs the ranks run in parallel).
 
-usage: python tools/slab_overhead.py [ranks] [K]
+usage: python tools/slab_overhead.py [ranks]
 """
 import json
 import os
@@ -28,7 +28,6 @@ from paper_1511_04292_b200.problems import config_fields, config_schedule  # noq
 
 def main():
     ranks = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-    K = int(sys.argv[2]) if len(sys.argv) > 2 else 16
     torch.cuda.set_device(0)
     f = config_fields("cfg3")
     p = GridProblem(spacing=(1.0,) * 3, u=f["u"], source=f["source"], center=f["center"],
@@ -37,16 +36,21 @@ def main():
     em = EmulatedRanks(p, ranks, 2)
     cur = em.run_chunk(0, w, 0, 8, 2)  # warm (TMA descriptors, attributes)
     torch.cuda.synchronize()
-    out = {"ranks": ranks, "fused_launches_per_rank": K}
-    # host enqueue cost behind a long sleep kernel
-    samples = []
-    for _ in range(5):
-        torch.cuda._sleep(2_000_000_000)  # ~1 s at 1.9 GHz
-        t0 = time.perf_counter()
-        cur = em.run_chunk(cur, w, 0, 2 * K, 2)
-        samples.append(time.perf_counter() - t0)
-        torch.cuda.synchronize()
-    host_us = min(samples) / (K * ranks) * 1e6
+    out = {"ranks": ranks}
+    # host enqueue cost behind a long sleep kernel, in calls short enough not
+    # to fill the launch queue (which would block the host on the GPU)
+    per_k = {}
+    for k in (1, 2, 4):
+        samples = []
+        for _ in range(5):
+            torch.cuda._sleep(200_000_000)  # ~0.1 s at 1.9 GHz
+            t0 = time.perf_counter()
+            cur = em.run_chunk(cur, w, 0, 2 * k, 2)
+            samples.append(time.perf_counter() - t0)
+            torch.cuda.synchronize()
+        per_k[k] = min(samples) / (k * ranks) * 1e6
+    out["host_us_per_fused_launch_per_rank_by_K"] = per_k
+    host_us = min(per_k.values())
     out["host_us_per_fused_launch_per_rank"] = host_us
     # device time per fused step: emulated ranks (serialised on one GPU)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
