@@ -82,7 +82,7 @@ __device__ __forceinline__ unsigned long long wait_ge(const unsigned long long *
 }
 
 template <int ND, bool VAR, bool RECIP, bool DEEP>
-__global__ void __launch_bounds__(32) gs_sweep(const __grid_constant__ GSParams p) {
+__global__ void __launch_bounds__(32, (DEEP || VAR) ? 1 : 12) gs_sweep(const __grid_constant__ GSParams p) {
   const int lane = threadIdx.x;
   const int s = blockIdx.x;
   const int64_t R = int64_t(s) * 32 + lane;
