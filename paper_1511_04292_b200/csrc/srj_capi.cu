@@ -832,7 +832,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     CUtensorMap tu, tf;
     int rc = plan_tmap(plan, &tu, cur, k3.box_cols, k3.box_rows);
     if (rc != SRJ_OK) return rc;
-    rc = plan_tmap(plan, &tf, f, k3.box_cols, k3.box_rows);
+    rc = plan_tmap(plan, &tf, f, k3.box_cols, k3.f_box_rows);
     if (rc != SRJ_OK) return rc;
     k3.launch(p, tu, tf, int(tiles * p.nstrips), st);
   } else {

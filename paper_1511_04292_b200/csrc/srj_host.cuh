@@ -18,6 +18,7 @@
 #include "srj_sweep2d.cuh"
 #include "srj_sweep3d.cuh"
 #include "srj_sweep3d_tb.cuh"
+#include "srj_sweep3d_rs.cuh"
 
 namespace srj_host {
 using namespace srj;
@@ -75,6 +76,15 @@ int cached_per_device(std::atomic<int> (&slot)[kMaxDevices], F &&f) {
   return n;
 }
 
+// SRJ_RS3D=0: use the shared-memory tile kernel (sweep3d_tb) for T=2 too
+inline bool rs3d_disabled() {
+  static const bool off = [] {
+    const char *e = getenv("SRJ_RS3D");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 inline int sm_count() {
   static std::atomic<int> cache[kMaxDevices];
   return cached_per_device(cache, [] {
@@ -117,6 +127,7 @@ struct Kernel3DTB {
                  cudaStream_t);
   int (*blocks_per_sm)();
   int tj, tk, box_cols, box_rows;
+  int f_box_rows;  // source box rows (sweep3d_rs loads fewer than for u)
 };
 
 Kernel3D pick3d(bool var, bool nl, bool recip);        // srj_k3d.cu

@@ -47,7 +47,7 @@ struct K3TB {
       return n > 0 ? n : 1;
     });
   }
-  static Kernel3DTB get() { return Kernel3DTB{launch, bps, B::TJ, B::TK, B::HS, B::HJ}; }
+  static Kernel3DTB get() { return Kernel3DTB{launch, bps, B::TJ, B::TK, B::HS, B::HJ, B::HJ}; }
 };
 
 template <int T, int BCF>
@@ -65,7 +65,42 @@ Kernel3DTB pick3d_tb_t(bool nl, bool recip, int bcf) {
   return nl ? K3TB<T, true, false>::get() : K3TB<T, false, false>::get();
 }
 
+// register-streaming T = 2 kernel (srj_sweep3d_rs.cuh): FIXED faces
+template <bool NL, bool RECIP>
+struct K3RS {
+  using B = RS3D;
+  static void configure() {
+    static std::atomic<uint64_t> done{0};
+    once_per_device(done, [] {
+      cudaFuncSetAttribute(sweep3d_rs<NL, RECIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(B::smem_bytes()));
+    });
+  }
+  static void launch(const Sweep3DTBParams &p, const CUtensorMap &tu, const CUtensorMap &tf,
+                     int blocks, cudaStream_t s) {
+    configure();
+    sweep3d_rs<NL, RECIP><<<blocks, B::THREADS, B::smem_bytes(), s>>>(p, tu, tf);
+  }
+  static int bps() {
+    static std::atomic<int> cache[kMaxDevices];
+    return cached_per_device(cache, [] {
+      configure();
+      int n = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d_rs<NL, RECIP>, B::THREADS,
+                                                    B::smem_bytes());
+      return n > 0 ? n : 1;
+    });
+  }
+  static Kernel3DTB get() {
+    return Kernel3DTB{launch, bps, B::TJ, B::TK, B::UC, B::UR, B::FR};
+  }
+};
+
 Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf) {
+  if (T == 2 && bcf == 0 && !rs3d_disabled()) {
+    if (recip) return nl ? K3RS<true, true>::get() : K3RS<false, true>::get();
+    return nl ? K3RS<true, false>::get() : K3RS<false, false>::get();
+  }
   switch (T) {
     case 2: return pick3d_tb_t<2>(nl, recip, bcf);
     default: return pick3d_tb_t<3>(nl, recip, bcf);
