@@ -11,7 +11,9 @@ import os
 __all__ = ["BC_KINDS", "LIB_PATH", "SrjFaceRule", "SrjLayout", "SrjPlanDesc", "SrjSlabPeer",
            "check", "load"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsrj.so")
+# SRJ_LIB_PATH: load another build (A/B timing of kernel variants; development only)
+LIB_PATH = os.environ.get("SRJ_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libsrj.so")
 
 SRJ_OK = 0
 SRJ_EINVAL = -1

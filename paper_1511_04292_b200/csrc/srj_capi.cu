@@ -834,7 +834,10 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     if (rc != SRJ_OK) return rc;
     rc = plan_tmap(plan, &tf, f, k3.box_cols, k3.f_box_rows);
     if (rc != SRJ_OK) return rc;
-    k3.launch(p, tu, tf, int(tiles * p.nstrips), st);
+    long blocks = tiles * p.nstrips;
+    if (k3.persistent)  // one CTA per resident slot, at least 8 planes each
+      blocks = std::max(1L, std::min(capacity, (tiles * rows + 7) / 8));
+    k3.launch(p, tu, tf, int(blocks), st);
   } else {
     Sweep3DParams p{};
     p.src = cur + ioff;

@@ -93,7 +93,10 @@ __device__ __forceinline__ double div_recip(double a, double c, double yh, doubl
   double q = __fma_rn(a, yh, __dmul_rn(a, yl));
   const double r = __fma_rn(-q, c, a);
   q = __fma_rn(r, yh, q);
-  const int hi = (__double2hiint(q) & 0x7fffffff) | (__double2hiint(a) & int(0x80000000));
+  // hi = (q.hi & 0x7fffffff) | (a.hi & 0x80000000): one bitwise select (LOP3)
+  int hi;
+  asm("lop3.b32 %0, %1, 0x7fffffff, %2, 0xE2;" : "=r"(hi) : "r"(__double2hiint(q)),
+      "r"(__double2hiint(a)));
   return __hiloint2double(hi, __double2loint(q));
 }
 

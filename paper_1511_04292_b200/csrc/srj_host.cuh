@@ -128,6 +128,7 @@ struct Kernel3DTB {
   int (*blocks_per_sm)();
   int tj, tk, box_cols, box_rows;
   int f_box_rows;  // source box rows (sweep3d_rs loads fewer than for u)
+  bool persistent; // sweep3d_rs: grid = resident CTAs, equal (tile, plane) shares
 };
 
 Kernel3D pick3d(bool var, bool nl, bool recip);        // srj_k3d.cu

@@ -47,7 +47,7 @@ struct K3TB {
       return n > 0 ? n : 1;
     });
   }
-  static Kernel3DTB get() { return Kernel3DTB{launch, bps, B::TJ, B::TK, B::HS, B::HJ, B::HJ}; }
+  static Kernel3DTB get() { return Kernel3DTB{launch, bps, B::TJ, B::TK, B::HS, B::HJ, B::HJ, false}; }
 };
 
 template <int T, int BCF>
@@ -92,7 +92,7 @@ struct K3RS {
     });
   }
   static Kernel3DTB get() {
-    return Kernel3DTB{launch, bps, B::TJ, B::TK, B::UC, B::UR, B::FR};
+    return Kernel3DTB{launch, bps, B::TJ, B::TK, B::UC, B::UR, B::FR, true};
   }
 };
 

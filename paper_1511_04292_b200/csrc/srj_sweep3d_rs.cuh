@@ -18,6 +18,7 @@
 // immediate.  Per stage-1 cell: 6 LDS + 1 STS; per stage-2 cell: 4 LDS + 1 STG
 // (sweep3d_tb: 8 LDS per cell and stage, all addresses recomputed per tick).
 //
+// Work: persistent CTAs over (tile, plane) segments (see the kernel head).
 // Tile (8 warps): stage 2 owns 14 (j) x 64 (k) cells; stage 1 covers the
 // 16 x 66 cone around it.  Warp w holds rows a = 2w, 2w+1 of the 16 stage-1
 // rows, lanes hold k = lane and lane + 32 (4 columns per thread); the 32
@@ -104,20 +105,45 @@ __global__ void __launch_bounds__(RS3D::THREADS, 2)
   double *win = ring_f + NS * B::F_TILE;
   uint64_t *bar = reinterpret_cast<uint64_t *>(win + 3 * B::W_TILE + WC);
 
+  // Persistent CTAs: the (tile, plane) units of the launch, tile-major, are
+  // split into gridDim.x equal contiguous shares; a share is one or two
+  // segments (a tile's planes [i0, i1)), each streamed like a strip.  Equal
+  // shares instead of whole strips keep every SM busy when the tile count
+  // does not fill whole waves (256^3: 76 tiles on 296 slots).
   const int ntiles = p.ntj * p.ntk;
-  const int tile = blockIdx.x % ntiles;
-  const int strip = blockIdx.x / ntiles;
-  if (strip >= p.nstrips) return;  // whole CTA exits together
+  const int rows = p.own_e - p.own_b;
+  const int64_t total = int64_t(ntiles) * rows;
+  const int64_t share = (total + gridDim.x - 1) / gridDim.x;
+  int64_t u_beg = int64_t(blockIdx.x) * share;
+  const int64_t u_end = min(u_beg + share, total);
+  if (u_beg >= u_end) return;  // whole CTA exits together
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+#pragma unroll 1
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  constexpr int NC = 4;
+  const double kc0 = p.kc[0], kc1 = p.kc[1], kc2 = p.kc[2], kc3 = p.kc[3], kc4 = p.kc[4],
+               kc5 = p.kc[5], kc6 = p.kc[6];
+  const double om1 = p.omega[0], om2 = p.omega[1];
+  double rmx1 = 0.0, rmx2 = 0.0;
+  int gt0 = 0;  // ticks of earlier segments: ring slot / mbarrier phase of tick it = gt0 + it
+
+#pragma unroll 1
+  while (u_beg < u_end) {
+  const int tile = int(u_beg / rows);
+  const int i0 = p.own_b + int(u_beg - int64_t(tile) * rows);
+  const int i1 = p.own_b + int(min(u_end, int64_t(tile + 1) * rows) - int64_t(tile) * rows);
+  u_beg = int64_t(tile) * rows + (i1 - p.own_b);
   const int tj = tile / p.ntk, tk = tile % p.ntk;
   const int jb = tj * B::TJ, kb = tk * B::TK;  // first owned (j, k)
-  const int i0 = p.own_b + strip * p.H;
-  const int i1 = min(i0 + p.H, p.own_e);
   const int rho_b = max(i0 - 2, p.ld_lo);
   const int nticks = i1 + 3 - rho_b;  // last tick: stage 2 emits plane i1 - 1
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  auto issue = [&](int q) {  // planes of tick q into ring slot q % NS
-    const int s = q % NS;
+  auto issue = [&](int q) {  // planes of tick q into ring slot (gt0 + q) % NS
+    const int s = (gt0 + q) % NS;
     const int plane = min(max(rho_b + q, p.ld_lo), p.ld_hi);
     const int row = p.tma_row0 + plane * p.rows_per_plane + jb;
     mbar_expect_tx(&bar[s], B::U_BYTES + B::F_BYTES);
@@ -125,9 +151,8 @@ __global__ void __launch_bounds__(RS3D::THREADS, 2)
     tma_box_2d(ring_f + s * B::F_TILE, &tm_f, p.tma_col0 + kb - 2, row - 1, &bar[s]);
   };
   if (tid == 0) {
-#pragma unroll 1
-    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
-    fence_mbar_init();
+    // the previous segment's last barrier ended every read of the slots
+    fence_proxy_async();
 #pragma unroll 1
     for (int q = 0; q < NS && q < nticks; ++q) issue(q);
   }
@@ -135,7 +160,6 @@ __global__ void __launch_bounds__(RS3D::THREADS, 2)
   // Column c = 0..3: stage-1 row a = 2*warp + (c >> 1), column b = lane +
   // 32*(c & 1); (j, k) = (jb - 1 + a, kb + b).  Column 4 (warp 0 only): the
   // stage-1 k-halo, a = lane & 15, b = lane < 16 ? -1 : 64.
-  constexpr int NC = 4;
   const int a0 = 2 * warp;
   const bool edge = warp == 0;
   const int ae = lane & 15, be = lane < 16 ? -1 : 64;
@@ -169,11 +193,6 @@ __global__ void __launch_bounds__(RS3D::THREADS, 2)
     for (int c = 0; c < NC; ++c) U[x][c] = S[x][c] = F[x][c] = 0.0;
     UE[x] = 0.0;
   }
-  double rmx1 = 0.0, rmx2 = 0.0;
-  const double kc0 = p.kc[0], kc1 = p.kc[1], kc2 = p.kc[2], kc3 = p.kc[3], kc4 = p.kc[4],
-               kc5 = p.kc[5], kc6 = p.kc[6];
-  const double om1 = p.omega[0], om2 = p.omega[1];
-  __syncthreads();
 
   // d = (om*rr)/c: double-word reciprocal (flagging numerators it cannot
   // take) or, in the fix-up pass, exact per cell
@@ -189,10 +208,11 @@ __global__ void __launch_bounds__(RS3D::THREADS, 2)
   auto tick = [&](auto phc, int it) {
     constexpr int PH = decltype(phc)::value;           // it % 3
     constexpr int P1 = (PH + 2) % 3, P2 = (PH + 1) % 3;  // ticks it-1, it-2 (it-3 = PH)
-    mbar_wait(&bar[it % NS], (it / NS) & 1);
-    const double *un = ring_u + (it % NS) * B::U_TILE;             // plane rho
-    const double *uo = ring_u + ((it + NS - 1) % NS) * B::U_TILE;  // plane rho - 1
-    const double *fo = ring_f + ((it + NS - 1) % NS) * B::F_TILE;  // source of rho - 1
+    const int g = gt0 + it;
+    mbar_wait(&bar[g % NS], (g / NS) & 1);
+    const double *un = ring_u + (g % NS) * B::U_TILE;             // plane rho
+    const double *uo = ring_u + ((g + NS - 1) % NS) * B::U_TILE;  // plane rho - 1
+    const double *fo = ring_f + ((g + NS - 1) % NS) * B::F_TILE;  // source of rho - 1
     double *wnew = win + PH * B::W_TILE;                           // stage 1 of this tick
     const double *w2 = win + P2 * B::W_TILE;                       // stage 1 of tick it - 2
     const int pl1 = rho_b + it - 1, pl2 = rho_b + it - 3;
@@ -280,6 +300,8 @@ __global__ void __launch_bounds__(RS3D::THREADS, 2)
     if (it + 2 >= nticks) break;
     tick(std::integral_constant<int, 2>{}, it + 2);
   }
+  gt0 += nticks;
+  }  // segments
 
   // per-step norms: dmax is monotone in rmax (constant centre)
   const double rm[2] = {warp_max(fabs(rmx1)), warp_max(fabs(rmx2))};

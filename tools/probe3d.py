@@ -59,10 +59,11 @@ def main():
     ap.add_argument("--steps", type=int, default=240)
     ap.add_argument("--fuse", type=int, default=2)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--workloads", default="cfg3,cfg5")
     a = ap.parse_args()
     mode = "tb" if os.environ.get("SRJ_RS3D", "1") == "0" else "rs"
     for n in [int(x) for x in a.sizes.split(",")]:
-        for wl in ("cfg3", "cfg5"):
+        for wl in a.workloads.split(","):
             r = run(wl, n, a.steps, a.fuse, a.reps)
             r["kernel"] = mode
             print(json.dumps(r), flush=True)
