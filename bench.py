@@ -75,6 +75,10 @@ WORKLOADS = {
 }
 
 
+# --secondary default: (timed cycles, warm-up cycles) per extra workload
+SECONDARY = {"cfg3": (3, 1), "cfg5": (10, 3), "cfg2": (3, 1), "cfg1": (20, 3)}
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -510,6 +514,55 @@ def measure_ttr(args, ws, rank, comm, shape, host):
             "api": "srj_solve(..., stop='residual_l2')", "n_gpus": ws}
 
 
+def measure_secondary(workload, steps, warmup):
+    """Device-resident GLUPS of another BASELINE config on this GPU (N=1), so
+    the default bench line also records the 3D kernels: ``steps`` full
+    M-cycles after ``warmup``, CUDA events on the grid's stream, clocks
+    sampled during the timed region."""
+    import torch
+
+    from paper_1511_04292_b200.engine import DeviceGrid
+    from paper_1511_04292_b200.problems import CONFIGS, config_fields, config_schedule
+
+    wl = WORKLOADS[workload]
+    shape = tuple(CONFIGS[workload]["shape"])
+    f = config_fields(workload, shape)
+    cyc = config_schedule(workload)
+    w, m = cyc.weight_sequence, cyc.m
+    grid = DeviceGrid(f["u"], f["source"], f["center"], f["lower"], f["upper"],
+                      kappa=f.get("kappa"))
+    T = wl["fuse"]
+    try:
+        cur, k = 0, 0
+        for _ in range(warmup):
+            cur = grid.run(cur, w, k, m, T)
+            k += m
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            ev0.record(grid.stream)
+            for _ in range(steps):
+                cur = grid.run(cur, w, k, m, T)
+                norms = grid.norms[:2 * m].view(m, 2).cpu().numpy()  # per-cycle host check
+                if not np.all(np.isfinite(norms)):
+                    raise RuntimeError(f"non-finite norms in the {workload} measurement")
+                k += m
+            ev1.record(grid.stream)
+            torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+    finally:
+        grid.close()
+    cells = int(np.prod(shape))
+    value = cells * m * steps / (ms * 1e-3) / 1e9
+    peak, _ = peaks()
+    return {"workload": wl["desc"], "value": value, "unit": "GLUPS", "steps": steps,
+            "warmup": warmup, "ms_per_step": ms / steps, "step": f"one full M-cycle ({m} sweeps)",
+            "fuse": T, "kernel": "sweep3d_rs<T=2> (register-streaming, persistent CTAs)",
+            "frac_of_hbm_roofline_single_sweep": value * BYTES_PER_UPDATE / peak,
+            "clocks": clk.summary()}
+
+
 def run_dry(args):
     """--dry-run: the launcher, rendezvous, rank-local inputs and collectives
     without kernels (gloo, CPU) -- exercised by tests/test_bench_launcher.py."""
@@ -674,6 +727,11 @@ def run_gpu(args):
         line["cpu_baseline"] = cpu
     if cpu_port:
         line["cpu_port"] = cpu_port
+    if ws == 1 and args.secondary:
+        # the 3D BASELINE configs on the same box, device-resident (the
+        # headline metric above is the --workload's)
+        line["other_workloads"] = [measure_secondary(x, *SECONDARY[x]) for x in
+                                   args.secondary.split(",") if x != args.workload]
     print(json.dumps(line), flush=True)
     return 0
 
@@ -691,6 +749,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttr", action="store_true")
+    ap.add_argument("--secondary", default="cfg3,cfg5",
+                    help="N=1: also time these workloads device-resident (empty: none)")
     ap.add_argument("--slab", action="store_true",
                     help="use the multi-GPU slab path even on one GPU (testing)")
     ap.add_argument("--dry-run", action="store_true",

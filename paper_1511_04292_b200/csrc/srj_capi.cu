@@ -399,7 +399,8 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
     if (desc->bc[a][0].kind == SRJ_BC_PERIODIC) p->bc_fusable = false;
   p->default_fuse = (desc->coef_mode == 0 && (!p->has_bc || p->bc_fusable))
                         ? (l.ndim == 2 ? 4 : 2)
-                        : 1;
+                        : 1;  // per-cell coefficients: the fused T=2 kernel (srj_sweep2d_vtb.cuh)
+                              // is no faster than one sweep per launch at 4096^2
   p->partials = nullptr;
   p->bc_scalars = nullptr;
   cudaError_t e = cudaMalloc(&p->partials, sizeof(double) * 2 * kResidBlocks);
@@ -708,6 +709,35 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
   const int rows = int(own_e - own_b);
   if (l.ndim == 2 && var && t == 1) {
     const int rc = launch_var2d(d, own_b, own_e, cur, nxt, f, ld_lo, ld_hi, om[0], norms, st);
+    if (rc != SRJ_OK) return rc;
+  } else if (l.ndim == 2 && var && t == 2 && !plan.has_bc) {
+    // two fused steps on per-cell coefficients (srj_sweep2d_vtb.cuh)
+    VarTB2DParams p{};
+    p.src = cur + ioff;
+    p.dst = nxt + ioff;
+    p.f = f + ioff;
+    p.act = d.act ? d.act + ioff : nullptr;
+    p.c = d.coef_arrays[0] + ioff;
+    p.am0 = d.coef_arrays[1] + ioff;
+    p.ap0 = d.coef_arrays[2] + ioff;
+    p.am1 = d.coef_arrays[3] + ioff;
+    p.ap1 = d.coef_arrays[4] + ioff;
+    p.pitch = l.pitch;
+    p.n0 = int(l.n[0]);
+    p.n1 = int(l.n[1]);
+    p.lo_c = lo_c;
+    p.hi_c = hi_c;
+    p.ld_lo = ld_lo;
+    p.ld_hi = ld_hi;
+    p.own_b = int(own_b);
+    p.own_e = int(own_e);
+    // last interior column (relative to the row origin) a double2 load may
+    // start at: element origin+1+col+1 stays inside the padded row
+    p.col_max = int(l.pitch - (l.origin + 1) - 2) & ~1;
+    p.omega[0] = om[0];
+    p.omega[1] = om[1];
+    p.norms = norms;
+    const int rc = launch_var2d_tb(p, nl, st);
     if (rc != SRJ_OK) return rc;
   } else if (l.ndim == 2) {
     Sweep2DParams p{};

@@ -19,6 +19,7 @@
 #include "srj_sweep3d.cuh"
 #include "srj_sweep3d_tb.cuh"
 #include "srj_sweep3d_rs.cuh"
+#include "srj_sweep2d_vtb.cuh"
 
 namespace srj_host {
 using namespace srj;
@@ -133,6 +134,8 @@ struct Kernel3DTB {
 
 Kernel3D pick3d(bool var, bool nl, bool recip);        // srj_k3d.cu
 Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf);  // srj_k3d.cu
+// fused T = 2 per-cell-coefficient 2D sweep (srj_kvar.cu); sets H/nbands/nstrips
+int launch_var2d_tb(VarTB2DParams p, bool nl, cudaStream_t st);
 int launch_gs(const GSParams &p, int nd, bool var, bool recip, int nstrips, cudaStream_t st);  // srj_kgs.cu
 
 }  // namespace srj_host

@@ -27,7 +27,9 @@ def fields(shape, masked, seed=0):
 
 
 FUSE = [int(x) for x in os.environ.get("VAR_FUSE", "1").split(",")]
-for shape, bpu in (((4096, 4096), 65), ((512, 512, 512), 81)):
+SHAPES = [tuple(int(v) for v in s.split("x")) for s in
+          os.environ.get("VAR_SHAPES", "4096x4096,512x512x512").split(",")]
+for shape, bpu in ((s, 65 if len(s) == 2 else 81) for s in SHAPES):
   for fuse in (FUSE if len(shape) == 2 else [1]):
     for masked in (False, True):
         u, s, c, lo, hi, mask = fields(shape, masked)
@@ -36,7 +38,7 @@ for shape, bpu in (((4096, 4096), 65), ((512, 512, 512), 81)):
         dev.run(0, w, 0, 8, fuse)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        steps = 40
+        steps = int(os.environ.get("VAR_STEPS", "40"))
         e0.record(dev.stream)
         dev.run(0, w, 0, steps, fuse)
         e1.record(dev.stream)
