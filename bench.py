@@ -151,8 +151,8 @@ def ncu_traffic(workload, fuse, cells):
     """DRAM bytes per launch from the committed ncu capture of the dominant
     kernel at this workload's size (profiles/), or None."""
     names = {("cfg2", 4096 * 4096): f"round1_ncu_sweep2d_T{fuse}.json",
-             ("cfg3", 512 ** 3): "round2_ncu_sweep3d_tb_T2_512.json",
-             ("cfg5", 256 ** 3): "round2_ncu_sweep3d_tb_T2_nl256.json"}
+             ("cfg3", 512 ** 3): "round2_ncu_sweep3d_rs_T2_512.json",
+             ("cfg5", 256 ** 3): "round2_ncu_sweep3d_rs_T2_nl256.json"}
     name = names.get((workload, cells))
     path = os.path.join(ROOT, "profiles", name) if name else None
     if not path or not os.path.exists(path):
@@ -682,7 +682,7 @@ def run_gpu(args):
     if ws > 1:
         launches = int(comm.sum_(np.array([float(launches)]))[0])
     gridname = ("sweep2d_tb<T=%d> (fused %d sweeps/launch)" % (T, T) if nd == 2 else
-                "sweep3d_tb<T=%d> (fused %d sweeps/launch, CTA tiles)" % (T, T))
+                "sweep3d_rs<T=%d> (fused %d sweeps/launch, register streaming)" % (T, T))
 
     e2e = None if args.e2e_steps <= 0 else measure_e2e(args, ws, rank, comm, shape,
                                                         sweeps, host)
