@@ -85,9 +85,12 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   int cur = 0;
   for (int s = 0; s <= p.nsteps; ++s) {
     cluster.sync();  // every CTA finished writing buffer `cur`
-    // ---- halo rows from the neighbours (interior columns only) ----------
-    const int last = C - 1;
     double *mine = buf[cur];
+    // step 0 relaxes the field as loaded: its halo rows came from memory and
+    // its ghosts are the caller's (the reference sweeps the given ghosts and
+    // refreshes only after each sweep, grids.py:557-558)
+    if (s > 0) {
+    // ---- halo rows from the neighbours (interior columns only) ----------
     if (rank > 0) {
       const double *up = cluster.map_shared_rank(buf[cur], rank - 1);
       const int urows = R;  // upper neighbour is full
@@ -151,6 +154,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
         at(cur, lr, side ? p.n1 : -1) = g;
       }
     }
+    }  // s > 0
     __syncthreads();
     if (s == p.nsteps) break;  // final buffer refreshed; write-out below
 

@@ -71,6 +71,16 @@ def main():
     ev1.record()
     torch.cuda.synchronize()
     out["one_rank_device_us_per_fused_step"] = ev0.elapsed_time(ev1) * 1e3 / (steps / 2)
+    # host cost of one plain fused launch (srj_plan_run, no exchange): the
+    # floor of the per-launch host cost, one kernel launch
+    samples = []
+    for _ in range(5):
+        torch.cuda._sleep(200_000_000)
+        t0 = time.perf_counter()
+        c = g.run(c, w, 0, 64, 2)
+        samples.append(time.perf_counter() - t0)
+        torch.cuda.synchronize()
+    out["host_us_per_plain_fused_launch"] = min(samples) / 32 * 1e6
     out["ratio_to_8gpu_launch_130us"] = host_us / 130.0
     print(json.dumps(out))
 
