@@ -1,0 +1,122 @@
+"""Seeded random problems built with the REFERENCE's own GridProblem, solved by
+the reference (``srj.grids.srj_solve``, numba, ``grids.py:642-687``) and by
+the GPU drop-in, compared bit for bit.
+
+Every case draws: 2D or 3D, a size that lands on one of the kernel paths
+(small-grid cluster, fused band, 3D register-streaming / tile, one sweep per
+launch), constant or per-cell coefficients, an optional mask, every boundary
+rule (with scalar or per-position face values), ghosts that may violate the
+rules at the start, the fused depth and chunk length of our side, and a
+tolerance that stops the solve inside a chunk (taken from a first reference
+run).  Skipped without ``baseline/_ref``.
+"""
+
+import copy
+import os
+
+import numpy as np
+import pytest
+
+from paper_1511_04292_b200 import grids as G
+
+from test_gpu_reference_dropin import REF, ref  # noqa: F401 - fixture
+
+pytestmark = pytest.mark.gpu
+
+KINDS = ("fixed", "mirror", "periodic", "face_dirichlet")
+
+
+def _face_shape(shape, ax):
+    return tuple(n for a, n in enumerate(shape) if a != ax)
+
+
+def _case(rg, seed):
+    rng = np.random.default_rng(7000 + seed)
+    nd = 2 if seed % 3 else 3
+    if nd == 2:
+        pick = int(rng.integers(0, 3))
+        shape = tuple(int(x) for x in (rng.integers(8, 120, 2) if pick == 0 else
+                                       rng.integers(300, 700, 2) if pick == 1 else
+                                       rng.integers(40, 300, 2)))
+    else:
+        shape = tuple(int(x) for x in rng.integers(6, 44, 3))
+    var = rng.random() < 0.5
+    masked = var and rng.random() < 0.4
+    if var:
+        center = 2.0 * nd + rng.random(shape)
+        lower = tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd))
+        upper = tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd))
+    else:
+        c = 2.0 * nd * (1.0 + rng.random())
+        center = np.full(shape, c)
+        lower = tuple(np.full(shape, -c / (2 * nd)) for _ in range(nd))
+        upper = tuple(np.full(shape, -c / (2 * nd)) for _ in range(nd))
+    bc = []
+    for ax in range(nd):
+        k = KINDS[int(rng.integers(0, 4))] if rng.random() < 0.6 else "fixed"
+        if k == "periodic":
+            bc.append((rg.BoundaryRule("periodic"), rg.BoundaryRule("periodic")))
+            continue
+        pair = []
+        for _ in range(2):
+            kk = KINDS[int(rng.choice([0, 1, 3]))] if rng.random() < 0.6 else "fixed"
+            if kk == "face_dirichlet":
+                vals = (rng.standard_normal(_face_shape(shape, ax)) if rng.random() < 0.5
+                        else float(rng.standard_normal()))
+                pair.append(rg.face_dirichlet(vals))
+            else:
+                pair.append(rg.BoundaryRule(kk))
+        bc.append(tuple(pair))
+    p = rg.GridProblem(spacing=(1.0,) * nd, u=rng.standard_normal(tuple(n + 2 for n in shape)),
+                       source=rng.standard_normal(shape), center=center, lower=lower,
+                       upper=upper, bc=tuple(bc),
+                       mask=(rng.random(shape) > 0.1) if masked else None)
+    if rng.random() < 0.5:  # ghosts that violate the rules at the start
+        p.u[...] = rng.standard_normal(p.u.shape)
+    weights = np.concatenate([[float(rng.uniform(2.0, 40.0))], rng.uniform(0.5, 1.0, 7)])
+    fuse = int(rng.integers(0, 5))
+    chunk = int(rng.integers(3, 40))
+    steps = int(rng.integers(8, 60))
+    return p, weights, fuse, chunk, steps
+
+
+class _Cycle:
+    def __init__(self, w):
+        self.weight_sequence = np.asarray(w, dtype=float)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SRJ_REF_RANDOM_CASES", "60"))))
+def test_reference_random_problem(ref, seed):  # noqa: F811
+    rg = ref[0]
+    p, w, fuse, chunk, steps = _case(rg, seed)
+    cyc = _Cycle(w)
+    # a tolerance that stops the reference inside the run (strictly between
+    # two recorded metrics), else the fixed step count
+    probe = copy.deepcopy(p)
+    h0, _ = rg.srj_solve(probe, cyc, 1e-300, max_iters=steps)
+    metric = np.asarray(h0.residual_inf)
+    tol = 1e-300
+    ok = np.isfinite(metric) & (metric > 0)
+    if ok.sum() > 4:
+        cand = np.sort(metric[ok])[: ok.sum() // 2]
+        tol = float(cand[-1]) * (1.0 + 1e-9)
+    a, b = copy.deepcopy(p), copy.deepcopy(p)
+    try:
+        h_ref, _ = rg.srj_solve(a, cyc, tol, max_iters=steps)
+        ref_err = None
+    except rg.DivergenceError as e:
+        h_ref, ref_err = e.history, e
+    try:
+        h_gpu, _ = G.srj_solve(b, cyc, tol, max_iters=steps, fuse=fuse, chunk=chunk)
+        gpu_err = None
+    except G.DivergenceError as e:
+        h_gpu, gpu_err = e.history, e
+    assert (ref_err is None) == (gpu_err is None), seed
+    assert h_gpu.iterations == h_ref.iterations, (seed, h_gpu.iterations, h_ref.iterations)
+    assert np.array_equal(np.asarray(h_gpu.residual_inf), np.asarray(h_ref.residual_inf),
+                          equal_nan=True), seed
+    assert np.array_equal(np.asarray(h_gpu.true_residual_inf),
+                          np.asarray(h_ref.true_residual_inf), equal_nan=True), seed
+    if ref_err is None:
+        assert h_gpu.converged == h_ref.converged, seed
+        assert np.array_equal(b.u, a.u, equal_nan=True), (seed, p.source.shape, fuse)
