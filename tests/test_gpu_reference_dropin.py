@@ -112,3 +112,24 @@ def test_reference_objects_through_the_gpu_drop_in(ref):
         h_ref, _ = rg.srj_solve(problem, cycle, tol, max_iters=200_000)
         h_gpu, _ = G.srj_solve(ours, cycle, tol, max_iters=200_000)
         _check(h_gpu, h_ref, ours, problem, name)
+
+
+def test_reference_single_sweeps_and_jacobi(ref):
+    """``weighted_jacobi_sweep`` (``grids.py:574-599``, both traversals) and
+    ``jacobi_solve`` (``:690-694``) on the reference's objects."""
+    rg, rp, rs, rt = ref
+    rng = np.random.default_rng(8)
+    gs = rp.grad_shafranov("B", 0.34, 64)
+    gs.u[...] = rng.standard_normal(gs.u.shape)
+    ours = copy.deepcopy(gs)
+    for k, (om, trav) in enumerate(((1.7, "forward"), (250.0, "reverse"), (0.6, "forward"))):
+        r_ref = rg.weighted_jacobi_sweep(gs, om, traversal=trav)
+        r_gpu = G.weighted_jacobi_sweep(ours, om, traversal=trav)
+        assert r_gpu == r_ref, k
+        assert np.array_equal(ours.u, gs.u), k
+    lap = rp.laplace2d_neumann(64)
+    lap.u[...] = rng.standard_normal(lap.u.shape)
+    ours = copy.deepcopy(lap)
+    h_ref, _ = rg.jacobi_solve(lap, 1e-4, max_iters=3000)
+    h_gpu, _ = G.jacobi_solve(ours, 1e-4, max_iters=3000)
+    _check(h_gpu, h_ref, ours, lap, "jacobi_solve laplace2d_neumann(64)")
