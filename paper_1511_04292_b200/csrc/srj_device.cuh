@@ -107,6 +107,13 @@ __device__ __forceinline__ bool recip_unsafe(double a) {
   return (e - 124u > 1798u) && !zero;  // exponent outside [-899, 899], nonzero
 }
 
+// Superset of recip_unsafe() in three integer ops (also flags a = 0): the
+// per-tick votes use it, the fix-up passes apply the exact test.
+__device__ __forceinline__ bool recip_maybe_unsafe(double a) {
+  const unsigned h2 = unsigned(__double2hiint(a)) << 1;  // exponent on top, sign dropped
+  return h2 - (124u << 21) > (1798u << 21) + ((1u << 21) - 1u);
+}
+
 // out of line: the IEEE division is the rare path and its inline expansion
 // would triple the size of the unrolled fast loop
 static __device__ __noinline__ double div_ieee(double a, double c) { return __ddiv_rn(a, c); }

@@ -184,7 +184,9 @@ __device__ __forceinline__ void stage2d(const Sweep2DParams &p, const double (&u
     double d;
     if (RECIP) {
       d = div_recip(num[v], p.kc, p.kinv, p.kinv_lo);
-      bad |= recip_unsafe(num[v]);
+      // superset test (also flags zero numerators) in fewer integer ops; the
+      // fix-up pass (fix_stage) applies the exact one
+      bad |= recip_maybe_unsafe(num[v]);
     } else {
       d = __ddiv_rn(num[v], cv[v]);
     }
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
           bc_ghost(p, 0, 1, prv[v], lane_col + v);                                            \
     }                                                                                         \
   }
-#define SRJ_STAGE(FASTV, EDGEV, SUBV)                                                                 \
+#define SRJ_STAGE(FASTV, EDGEV, SUBV, CNTV)                                                           \
   _Pragma("unroll") for (int t = T; t >= 1; --t) {                                            \
     const int fg = g + ((ph - 2 * t) >= 0 ? 0 : -((2 * t - ph + G - 1) / G));                 \
     const int fr = ph - 2 * t + G * (g - fg);                                                 \
@@ -388,7 +390,8 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
                                       w[t][(ph + 1) % 3],                                     \
                                       w[t][(ph + 2) % 3], frow, rho - 2 * t, p.omega[t - 1],  \
                                       lane_col, i0, i1, own_c0, own_c1, f_lo, f_hi, colact,   \
-                                      rho - 2 * t >= i0 && rho - 2 * t < i1, t >= 2 ? bcm : 0u,  \
+                                      CNTV || (rho - 2 * t >= i0 && rho - 2 * t < i1),           \
+                                      t >= 2 ? bcm : 0u,                                         \
                                       dst, num[t],                                            \
                                       rmx[t - 1], dmx[t - 1], bad);                           \
   }                                                                                           \
@@ -399,16 +402,20 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
                                  dst);                                                        \
     }                                                                                         \
   }
-      if (band_interior && fast_rows) {
-        SRJ_STAGE(true, false, 0)
+      // every stage row of the tick inside the strip: no per-cell count gate
+      const bool all_cnt = rho - 2 * T >= i0 && rho - 2 < i1;
+      if (band_interior && fast_rows && all_cnt) {
+        SRJ_STAGE(true, false, 0, true)
+      } else if (band_interior && fast_rows) {
+        SRJ_STAGE(true, false, 0, false)
       } else if (band_edge && fast_rows) {
         if (BCF && warp_sub) {
-          SRJ_STAGE(true, true, BCF)
+          SRJ_STAGE(true, true, BCF, false)
         } else {
-          SRJ_STAGE(true, true, 0)
+          SRJ_STAGE(true, true, 0, false)
         }
       } else {
-        SRJ_STAGE(false, false, BCF)
+        SRJ_STAGE(false, false, BCF, false)
         if (BCF) SRJ_BCFIX
       }
 #undef SRJ_BCFIX

@@ -59,13 +59,6 @@ struct RS3D {
   }
 };
 
-// Superset of recip_unsafe() in three integer ops (also flags a = 0): the
-// per-tick vote uses it, the fix-up pass applies the exact test.
-__device__ __forceinline__ bool recip_maybe_unsafe(double a) {
-  const unsigned h2 = unsigned(__double2hiint(a)) << 1;  // exponent on top, sign dropped
-  return h2 - (124u << 21) > (1798u << 21) + ((1u << 21) - 1u);
-}
-
 // act ? a : b without letting the compiler turn the select into a branch
 // around the computation of a (the FP64 chains of the columns must interleave)
 __device__ __forceinline__ double sel(bool act, double a, double b) {
