@@ -150,7 +150,7 @@ class ClockSampler:
 def ncu_traffic(workload, fuse, cells):
     """DRAM bytes per launch from the committed ncu capture of the dominant
     kernel at this workload's size (profiles/), or None."""
-    names = {("cfg2", 4096 * 4096): f"round1_ncu_sweep2d_T{fuse}.json",
+    names = {("cfg2", 4096 * 4096): f"round2_ncu_sweep2d_T{fuse}.json",
              ("cfg3", 512 ** 3): "round2_ncu_sweep3d_rs_T2_512.json",
              ("cfg5", 256 ** 3): "round2_ncu_sweep3d_rs_T2_nl256.json"}
     name = names.get((workload, cells))
