@@ -210,7 +210,8 @@ struct srj_plan {
   bool has_bc;       // some face is not FIXED: refresh ghosts after each launch
   bool bc_fusable;   // ...and none is PERIODIC: fused launches form the ghosts on chip
   int default_fuse;
-  double *partials;  // [kResidBlocks][2] device scratch
+  double *partials;  // [resid_blocks][2] device scratch
+  int resid_blocks;  // 4 x SMs (fixed per device, so a fixed reduction order)
   double *row_parts = nullptr;  // 3D per-(i,j)-row residual partials (srj_plan_residual_layers)
   int64_t row_parts_cap = 0;
   double *bc_scalars;  // [3][2] device copies of the faces' scalar values (fused BCs)
@@ -403,7 +404,8 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
                               // is no faster than one sweep per launch at 4096^2
   p->partials = nullptr;
   p->bc_scalars = nullptr;
-  cudaError_t e = cudaMalloc(&p->partials, sizeof(double) * 2 * kResidBlocks);
+  p->resid_blocks = std::min(4 * sm_count(), kResidBlocksMax);
+  cudaError_t e = cudaMalloc(&p->partials, sizeof(double) * 2 * p->resid_blocks);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "cudaMalloc(partials)");
@@ -1108,12 +1110,12 @@ int srj_plan_residual(srj_plan *plan, const double *u, double *d_out, void *stre
   const bool nl = d.kappa != nullptr, var = d.coef_mode == 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (var)
-    nl ? residual_partial<true, true><<<kResidBlocks, kResidThreads, 0, st>>>(p)
-       : residual_partial<true, false><<<kResidBlocks, kResidThreads, 0, st>>>(p);
+    nl ? residual_partial<true, true><<<plan->resid_blocks, kResidThreads, 0, st>>>(p)
+       : residual_partial<true, false><<<plan->resid_blocks, kResidThreads, 0, st>>>(p);
   else
-    nl ? residual_partial<false, true><<<kResidBlocks, kResidThreads, 0, st>>>(p)
-       : residual_partial<false, false><<<kResidBlocks, kResidThreads, 0, st>>>(p);
-  residual_final<<<1, 32, 0, st>>>(plan->partials, kResidBlocks, d_out);
+    nl ? residual_partial<false, true><<<plan->resid_blocks, kResidThreads, 0, st>>>(p)
+       : residual_partial<false, false><<<plan->resid_blocks, kResidThreads, 0, st>>>(p);
+  residual_final<<<1, 32, 0, st>>>(plan->partials, plan->resid_blocks, d_out);
   SRJ_CUDA(cudaGetLastError());
   return SRJ_OK;
 }

@@ -27,7 +27,7 @@ struct ResidParams {
 };
 
 constexpr int kResidThreads = 256;
-constexpr int kResidBlocks = 592;  // 4 x 148 SMs; fixed => fixed reduction order
+constexpr int kResidBlocksMax = 4096;  // grid = min(4 x SMs, this): fixed per device
 
 template <bool VAR, bool NL>
 __global__ void __launch_bounds__(kResidThreads) residual_partial(const __grid_constant__ ResidParams p) {
