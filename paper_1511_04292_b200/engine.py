@@ -13,6 +13,7 @@ CPU path: constructing a DeviceGrid without a CUDA device raises.
 """
 
 import ctypes
+import warnings
 
 import numpy as np
 
@@ -193,11 +194,42 @@ class DeviceGrid:
         self._keep.append(t)
         return t
 
-    def _upload_interior(self, host, dev, esize):
-        _lib.check(self.lib.srj_upload_interior(
-            ctypes.byref(self.layout), host.ctypes.data_as(ctypes.c_void_p),
-            ctypes.c_void_p(dev.data_ptr()), esize, self._sp), "srj_upload_interior")
+    # Host <-> device copies of the padded layout (srj_layout, include/srj.h):
+    # one contiguous transfer of the dense host array, then a device-side
+    # scatter / gather through a strided view of the padded buffer.  The C
+    # ABI's srj_upload_field / srj_upload_interior / srj_download_field do the
+    # same with row-wise 2D copies (one per plane for 3D interiors), which the
+    # copy engines run at well under the PCIe rate for 2-4 KB rows.
+    def _field_view(self, t):
+        l = self.layout
+        last = int(l.n[l.ndim - 1]) + 2
+        rows = (int(l.n[0]) + 2) * ((int(l.n[1]) + 2) if l.ndim == 3 else 1)
+        off = int(l.origin) + (int(l.halo0) - 1) * int(l.plane)
+        return t.as_strided((rows, last), (int(l.pitch), 1), t.storage_offset() + off)
+
+    def _interior_view(self, t):
+        l = self.layout
+        if l.ndim == 2:
+            off = int(l.origin) + int(l.halo0) * int(l.plane) + 1
+            return t.as_strided((int(l.n[0]), int(l.n[1])), (int(l.pitch), 1),
+                                t.storage_offset() + off)
+        off = int(l.origin) + int(l.halo0) * int(l.plane) + int(l.pitch) + 1
+        return t.as_strided((int(l.n[0]), int(l.n[1]), int(l.n[2])),
+                            (int(l.plane), int(l.pitch), 1), t.storage_offset() + off)
+
+    def _scatter(self, host, view):
+        torch = self.torch
+        with warnings.catch_warnings():  # read-only host arrays are only read
+            warnings.simplefilter("ignore", UserWarning)
+            src = torch.from_numpy(host).reshape(view.shape)
+        with torch.cuda.stream(self.stream):
+            staging = torch.empty(view.shape, dtype=view.dtype, device=self.device)
+            staging.copy_(src, non_blocking=True)
+            view.copy_(staging)
         self.stream.synchronize()  # host array may be a temporary
+
+    def _upload_interior(self, host, dev, esize):
+        self._scatter(host, self._interior_view(dev))
 
     def upload_field(self, host, dev):
         with self._on():
@@ -209,10 +241,7 @@ class DeviceGrid:
             self._upload_interior(_contig(host, np.float64), self.f_dev, 8)
 
     def _upload_field(self, host, dev):
-        _lib.check(self.lib.srj_upload_field(
-            ctypes.byref(self.layout), host.ctypes.data_as(ctypes.c_void_p),
-            ctypes.c_void_p(dev.data_ptr()), self._sp), "srj_upload_field")
-        self.stream.synchronize()
+        self._scatter(host, self._field_view(dev))
 
     def download_field(self, idx, host):
         """Copy field buffer ``idx`` into the ghosted host array (in place)."""
@@ -221,10 +250,10 @@ class DeviceGrid:
             self.download_field(idx, tmp)
             host[...] = tmp
             return
-        with self._on():
-            _lib.check(self.lib.srj_download_field(
-                ctypes.byref(self.layout), ctypes.c_void_p(self.fields[idx].data_ptr()),
-                host.ctypes.data_as(ctypes.c_void_p), self._sp), "srj_download_field")
+        torch = self.torch
+        with self._on(), torch.cuda.stream(self.stream):
+            dense = self._field_view(self.fields[idx]).contiguous()  # device gather
+            torch.from_numpy(host).view(dense.shape).copy_(dense, non_blocking=True)
         self.stream.synchronize()
 
     # -------------------------------------------------------------- compute
