@@ -9,7 +9,8 @@ static int vtb_bps() {
   static std::atomic<int> cache[kMaxDevices];
   return cached_per_device(cache, [] {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_vtb<NL>, kWarps2DVTB * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_vtb<NL>, kWarps2DVTB * 32,
+                                                  kVTBSmem);
     return n > 0 ? n : 1;
   });
 }
@@ -36,9 +37,9 @@ int launch_var2d_tb(VarTB2DParams p, bool nl, cudaStream_t st) {
   const long warps = long(p.nbands) * p.nstrips;
   const int blocks = int((warps + kWarps2DVTB - 1) / kWarps2DVTB);
   if (nl)
-    sweep2d_vtb<true><<<blocks, kWarps2DVTB * 32, 0, st>>>(p);
+    sweep2d_vtb<true><<<blocks, kWarps2DVTB * 32, kVTBSmem, st>>>(p);
   else
-    sweep2d_vtb<false><<<blocks, kWarps2DVTB * 32, 0, st>>>(p);
+    sweep2d_vtb<false><<<blocks, kWarps2DVTB * 32, kVTBSmem, st>>>(p);
   SRJ_CUDA(cudaGetLastError());
   return SRJ_OK;
 }

@@ -4,18 +4,23 @@
 //
 // The one-sweep kernel (srj_sweep2d_var.cuh) is HBM-bound at 65 B per update
 // (u, s, c, four coefficients, the mask byte, u').  Fusing two steps reads the
-// seven input arrays once per two updates (32.5 B/update):
-//   * a warp streams a 64-column band down a strip of rows (2 cells per lane,
-//     double2 loads); bands overlap by 2 columns per side (stage 1 relaxes
-//     band columns 1..62, stage 2 the owned columns 2..61; the overlap is
-//     recomputed, never stored);
-//   * tick rho: stage 1 relaxes row rho-1 from u rows rho-2..rho (registers,
-//     west/east by shuffle), stage 2 relaxes row rho-3 from the stage-1 rows
-//     rho-4..rho-2 (registers, a 3-row ring); no shared memory, no barrier;
-//   * everything the next tick needs -- u of row rho+1, the source,
-//     coefficients and mask of row rho (stage 1) and of row rho-2 (stage 2) --
-//     is loaded one tick ahead; the stage-2 operands were read two ticks
-//     earlier by this warp, so their second read hits L1/L2, not HBM.
+// input arrays once per two updates (32.5 B/update):
+//   * a warp streams a 64-column band down a strip of rows (2 cells per lane);
+//     bands overlap by 2 columns per side (stage 1 relaxes band columns
+//     1..62, stage 2 the owned columns 2..61; the overlap is recomputed,
+//     never stored);
+//   * tick rho: stage 1 relaxes row rho-1 from u rows rho-2..rho (west/east
+//     by shuffle), stage 2 relaxes row rho-3 from the stage-1 rows
+//     rho-4..rho-2 (a 3-row register ring); no barrier;
+//   * the seven arrays of a row (u, source, c, am0, ap0, am1, ap1) reach
+//     shared memory by per-lane asynchronous copies (cp.async, 16 B = the
+//     lane's two cells per array) three rows ahead, into a 7-row ring per warp
+//     (rows rho-3 .. rho+3); stage 2 re-reads row rho-3's coefficients from
+//     the ring, so every input byte crosses HBM once.  A lane only reads what
+//     it copied itself, so cp.async.wait_group is the only synchronisation,
+//     and no prefetch lives in registers (the first version prefetched one
+//     row into registers: 164 registers, 12 warps/SM, latency-bound at 86
+//     GLUPS).
 // Division is the IEEE one (the centre varies); dmax and rmax per cell.
 // Inactive (masked) cells, ghost columns and rows outside [lo_c, hi_c) pass
 // their value through; only owned rows and columns are stored and counted.
@@ -41,15 +46,31 @@ struct VarTB2DParams {
   double *norms;      // [2][2]: (dmax, rmax) per step
 };
 
-constexpr int kWarps2DVTB = 4;
-constexpr int kVTBOwn = 60;  // owned columns per band
+constexpr int kWarps2DVTB = 1;   // one warp per CTA: the ring is per warp
+constexpr int kVTBOwn = 60;      // owned columns per band
+constexpr int kVTBArrays = 7;    // u, f, c, am0, ap0, am1, ap1
+constexpr int kVTBRing = 7;      // rows rho-3 .. rho+3
+constexpr int kVTBAhead = 3;     // rows in flight beyond the current one
+constexpr size_t kVTBSmem = size_t(kVTBRing) * kVTBArrays * 32 * 16;  // 25,088 B per warp
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 template <bool NL>
 __global__ void __launch_bounds__(kWarps2DVTB * 32)
     sweep2d_vtb(const __grid_constant__ VarTB2DParams p) {
-  const int warp = threadIdx.x >> 5;
+  extern __shared__ __align__(16) double2 vtb_ring[];  // [slot][array][lane]
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kWarps2DVTB + warp;
+  const int gw = blockIdx.x;
   const int band = gw % p.nbands;
   const int strip = gw / p.nbands;
   double rmx[2] = {0.0, 0.0}, dmx[2] = {0.0, 0.0};
@@ -61,48 +82,46 @@ __global__ void __launch_bounds__(kWarps2DVTB * 32)
     const bool in0 = col >= 0 && col < p.n1, in1 = col + 1 >= 0 && col + 1 < p.n1;
     const bool own_l = lane >= 1 && lane <= 30;  // band columns 2..61
     const int64_t pitch = p.pitch;
-    auto ld2 = [](const double *a) { return __ldg(reinterpret_cast<const double2 *>(a)); };
-    auto mask2 = [&](int64_t o) -> unsigned {
+    const double *arr[kVTBArrays] = {p.src, p.f, p.c, p.am0, p.ap0, p.am1, p.ap1};
+    auto rowc = [&](int r) { return min(max(r, p.ld_lo), p.ld_hi); };
+    auto slot_of = [&](int r) { return (r - i0 + 3 * kVTBRing) % kVTBRing; };  // r >= i0 - 3
+    auto ring = [&](int r, int k) -> double2 {
+      return vtb_ring[(slot_of(r) * kVTBArrays + k) * 32 + lane];
+    };
+    auto issue = [&](int r) {  // row r of the seven arrays -> its ring slot (one commit group)
+      const int64_t o = int64_t(rowc(r)) * pitch + colc;
+      double2 *dst = vtb_ring + slot_of(r) * kVTBArrays * 32 + lane;
+#pragma unroll
+      for (int k = 0; k < kVTBArrays; ++k) cp_async16(dst + k * 32, arr[k] + o);
+      cp_async_commit();
+    };
+    auto mask2 = [&](int r) -> unsigned {
       if (!p.act) return 3u;
-      const unsigned short m = __ldg(reinterpret_cast<const unsigned short *>(p.act + o));
+      const unsigned short m = __ldg(
+          reinterpret_cast<const unsigned short *>(p.act + int64_t(rowc(r)) * pitch + colc));
       return (m & 0xffu ? 1u : 0u) | (m >> 8 ? 2u : 0u);
     };
-    auto rowc = [&](int r) { return min(max(r, p.ld_lo), p.ld_hi); };
-    struct Coef {
-      double2 f, c, a0, b0, a1, b1;
-      unsigned mk;
-    };
-    auto load_coef = [&](int r) {
-      const int64_t o = int64_t(rowc(r)) * pitch + colc;
-      Coef k;
-      k.f = ld2(p.f + o);
-      k.c = ld2(p.c + o);
-      k.a0 = ld2(p.am0 + o);
-      k.b0 = ld2(p.ap0 + o);
-      k.a1 = ld2(p.am1 + o);
-      k.b1 = ld2(p.ap1 + o);
-      k.mk = mask2(o);
-      return k;
-    };
-    const double *u = p.src + colc;
-    // one relaxation of the lane's two cells of row r: (y, counted r, counted d)
+    // one relaxation of the lane's two cells of row r with the coefficients
+    // of ring row r: returns the new pair, counts owned cells
     auto relax_row = [&](int t, int r, const double2 &um, const double2 &uc, const double2 &ud,
-                         const Coef &k, double2 &y) {
-      double w = __shfl_up_sync(kFull, uc.y, 1);
-      double e = __shfl_down_sync(kFull, uc.x, 1);
+                         unsigned mk) {
+      const double2 f = ring(r, 1), c = ring(r, 2), a0 = ring(r, 3), b0 = ring(r, 4),
+                    a1 = ring(r, 5), b1 = ring(r, 6);
+      const double w = __shfl_up_sync(kFull, uc.y, 1);
+      const double e = __shfl_down_sync(kFull, uc.x, 1);
       const bool row_ok = r >= p.lo_c && r < p.hi_c;
       const bool cnt = own_l && r >= i0 && r < i1;
       const double ucv[2] = {uc.x, uc.y}, umv[2] = {um.x, um.y}, udv[2] = {ud.x, ud.y},
-                   fv[2] = {k.f.x, k.f.y}, cv[2] = {k.c.x, k.c.y}, a0v[2] = {k.a0.x, k.a0.y},
-                   b0v[2] = {k.b0.x, k.b0.y}, a1v[2] = {k.a1.x, k.a1.y},
-                   b1v[2] = {k.b1.x, k.b1.y}, wv[2] = {w, uc.x}, ev[2] = {uc.y, e};
+                   fv[2] = {f.x, f.y}, cv[2] = {c.x, c.y}, a0v[2] = {a0.x, a0.y},
+                   b0v[2] = {b0.x, b0.y}, a1v[2] = {a1.x, a1.y}, b1v[2] = {b1.x, b1.y},
+                   wv[2] = {w, uc.x}, ev[2] = {uc.y, e};
       double yv[2];
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         // lane 0's west / lane 31's east neighbour is outside the band: those
         // two cells are never needed by stage 2 of an owned column
         const bool edge = (v == 0 && lane == 0) || (v == 1 && lane == 31);
-        const bool act = row_ok && !edge && (v == 0 ? in0 : in1) && ((k.mk >> v) & 1u);
+        const bool act = row_ok && !edge && (v == 0 ? in0 : in1) && ((mk >> v) & 1u);
         const double s = NL ? nl_source(fv[v], ucv[v]) : fv[v];
         const double rr = resid5(s, cv[v], ucv[v], a0v[v], umv[v], b0v[v], udv[v], a1v[v], wv[v],
                                  b1v[v], ev[v]);
@@ -113,27 +132,24 @@ __global__ void __launch_bounds__(kWarps2DVTB * 32)
           acc_absmax(dmx[t], d);
         }
       }
-      y = make_double2(yv[0], yv[1]);
+      return make_double2(yv[0], yv[1]);
     };
 
-    // tick rho: stage 1 -> row rho-1, stage 2 -> row rho-3
-    const int rb = i0;
-    double2 U0 = ld2(u + int64_t(rowc(rb - 2)) * pitch);  // u rows rho-2, rho-1, rho
-    double2 U1 = ld2(u + int64_t(rowc(rb - 1)) * pitch);
-    double2 U2 = ld2(u + int64_t(rowc(rb)) * pitch);
-    Coef K1 = load_coef(rb - 1), K2 = load_coef(rb - 3);  // stage-1 / stage-2 rows
+    // prologue: rows i0-3 .. i0+2 in flight (the ring holds i0-3 .. i0+3)
+#pragma unroll 1
+    for (int r = i0 - 3; r < i0 + kVTBAhead; ++r) issue(r);
     double2 S0 = make_double2(0.0, 0.0), S1 = S0, S2 = S0;  // stage 1 of rows rho-4..rho-2
+    unsigned mk1 = mask2(i0 - 1), mk2 = mask2(i0 - 3);      // masks of rows rho-1, rho-3
     const bool st0 = own_l && in0, st1 = own_l && in1;
 #pragma unroll 1
-    for (int rho = rb; rho <= i1 + 2; ++rho) {
-      // prefetch for tick rho+1
-      const double2 Un = ld2(u + int64_t(rowc(rho + 1)) * pitch);
-      const Coef K1n = load_coef(rho), K2n = load_coef(rho - 2);
+    for (int rho = i0; rho <= i1 + 2; ++rho) {
+      issue(rho + kVTBAhead);
+      cp_async_wait<kVTBAhead>();  // rows <= rho have landed
+      const unsigned mk1n = mask2(rho), mk2n = mask2(rho - 2);
       // stage 2: row rho-3 from stage-1 rows rho-4, rho-3, rho-2
       const int r2 = rho - 3;
       if (r2 >= i0) {
-        double2 y;
-        relax_row(1, r2, S0, S1, S2, K2, y);
+        const double2 y = relax_row(1, r2, S0, S1, S2, mk2);
         double *out = p.dst + int64_t(r2) * pitch + col;
         if (st0 && st1) {
           *reinterpret_cast<double2 *>(out) = y;
@@ -143,17 +159,15 @@ __global__ void __launch_bounds__(kWarps2DVTB * 32)
         }
       }
       // stage 1: row rho-1 from u rows rho-2, rho-1, rho
-      double2 s1;
-      relax_row(0, rho - 1, U0, U1, U2, K1, s1);
-      U0 = U1;
-      U1 = U2;
-      U2 = Un;
+      const double2 s1 = relax_row(0, rho - 1, ring(rho - 2, 0), ring(rho - 1, 0), ring(rho, 0),
+                                   mk1);
       S0 = S1;
       S1 = S2;
       S2 = s1;
-      K1 = K1n;
-      K2 = K2n;
+      mk1 = mk1n;
+      mk2 = mk2n;
     }
+    cp_async_wait<0>();
   }
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
