@@ -493,7 +493,7 @@ def measure_ttr(args, ws, rank, comm, shape, host):
                           bc=((G.FIXED, G.FIXED),) * nd, **kw)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        hist, _ = G.srj_solve(p, cyc, tol, stop="residual_l2", max_iters=200 * cyc.m)
+        hist, _ = G.srj_solve(p, cyc, tol, stop="residual_l2", max_iters=2000 * cyc.m)
         dt = time.perf_counter() - t0
     else:
         from paper_1511_04292_b200 import distributed as D
@@ -504,7 +504,7 @@ def measure_ttr(args, ws, rank, comm, shape, host):
         comm.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        hist, _ = D.srj_solve(sp, cyc, tol, stop="residual_l2", max_iters=200 * cyc.m)
+        hist, _ = D.srj_solve(sp, cyc, tol, stop="residual_l2", max_iters=2000 * cyc.m)
         dt = float(comm.max_(np.array([time.perf_counter() - t0]))[0])
     return {"tol": tol, "rule": "relative L2 of the true residual ||s - A u||_2 / ||s||_2 "
                                 "(cfg5: / initial residual), checked every M-cycle",
