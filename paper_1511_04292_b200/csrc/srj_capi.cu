@@ -606,7 +606,9 @@ static bool cluster_fits(const srj_plan &plan, int &C, int &R) {
   C = std::min(kClusterMax, n0);
   R = (n0 + C - 1) / C;
   C = (n0 + R - 1) / R;
-  if (R > kTY * kMaxA || l.n[1] > kTX * kMaxB) return false;  // register tiling limits
+  // cells per CTA <= 16 x 1024 threads (the row division by n1_magic is exact
+  // for them); n1 >= 2 keeps ceil(2^32 / n1) in 32 bits
+  if (R > kTY * kMaxA || l.n[1] > kTX * kMaxB || l.n[1] < 2) return false;
   const size_t bytes = 2 * size_t(R + 2) * size_t(l.n[1] + 2) * 8;
   return bytes <= 200 * 1024 && cluster_schedulable(plan, C, R);
 }
@@ -673,6 +675,7 @@ static int run_cluster2d(srj_plan &plan, const double *src, double *dst, const d
     }
   p.omegas = plan.d_omegas;
   p.nsteps = int(nsteps);
+  p.n1_magic = unsigned(((uint64_t(1) << 32) + uint64_t(l.n[1]) - 1) / uint64_t(l.n[1]));
   p.norms = d_norms;
   const size_t smem = 2 * size_t(R + 2) * size_t(p.sp) * 8;
   p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
