@@ -38,8 +38,10 @@ def _case(rg, seed):
         shape = tuple(int(x) for x in (rng.integers(8, 120, 2) if pick == 0 else
                                        rng.integers(300, 700, 2) if pick == 1 else
                                        rng.integers(40, 300, 2)))
-    else:
-        shape = tuple(int(x) for x in rng.integers(6, 44, 3))
+    else:  # mostly small; some span several 14 x 64 tiles of the 3D T=2 kernel
+        big = rng.random() < 0.3
+        shape = tuple(int(x) for x in (rng.integers(60, 130, 3) if big else
+                                       rng.integers(6, 44, 3)))
     var = rng.random() < 0.5
     masked = var and rng.random() < 0.4
     if var:
