@@ -214,6 +214,7 @@ struct srj_plan {
   int resid_blocks;  // 4 x SMs (fixed per device, so a fixed reduction order)
   double *row_parts = nullptr;  // 3D per-(i,j)-row residual partials (srj_plan_residual_layers)
   int64_t row_parts_cap = 0;
+  double *vtb_yh = nullptr, *vtb_yl = nullptr;  // per-cell reciprocal of c (sweep2d_vtb)
   double *bc_scalars;  // [3][2] device copies of the faces' scalar values (fused BCs)
   // small-grid cluster path: per-chunk omegas (device + pinned staging)
   double *d_omegas = nullptr, *h_omegas = nullptr;
@@ -400,8 +401,13 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
     if (desc->bc[a][0].kind == SRJ_BC_PERIODIC) p->bc_fusable = false;
   p->default_fuse = (desc->coef_mode == 0 && (!p->has_bc || p->bc_fusable))
                         ? (l.ndim == 2 ? 4 : 2)
-                        : 1;  // per-cell coefficients: the fused T=2 kernel (srj_sweep2d_vtb.cuh)
-                              // is no faster than one sweep per launch at 4096^2
+                        // per-cell coefficients (2D, FIXED faces): the fused T=2 kernel
+                        // (srj_sweep2d_vtb.cuh) from 2M cells up, where it beats one sweep
+                        // per launch
+                        : (desc->coef_mode == 1 && l.ndim == 2 && !p->has_bc &&
+                                   l.n[0] * l.n[1] >= (int64_t(1) << 21)
+                               ? 2
+                               : 1);
   p->partials = nullptr;
   p->bc_scalars = nullptr;
   p->resid_blocks = std::min(4 * sm_count(), kResidBlocksMax);
@@ -464,6 +470,8 @@ int srj_plan_destroy(srj_plan *p) {
   if (p->gs_prog) cudaFree(p->gs_prog);
   if (p->partials) cudaFree(p->partials);
   if (p->row_parts) cudaFree(p->row_parts);
+  if (p->vtb_yh) cudaFree(p->vtb_yh);
+  if (p->vtb_yl) cudaFree(p->vtb_yl);
   if (p->bc_scalars) cudaFree(p->bc_scalars);
   if (p->d_omegas) cudaFree(p->d_omegas);
   if (p->h_omegas) cudaFreeHost(p->h_omegas);
@@ -727,6 +735,19 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     p.ap0 = d.coef_arrays[2] + ioff;
     p.am1 = d.coef_arrays[3] + ioff;
     p.ap1 = d.coef_arrays[4] + ioff;
+    if (!plan.vtb_yh) {  // first fused per-cell launch: reciprocals of the centre
+      const size_t bytes = sizeof(double) * size_t(l.elems);
+      SRJ_CUDA(cudaMalloc(&plan.vtb_yh, bytes));
+      SRJ_CUDA(cudaMalloc(&plan.vtb_yl, bytes));
+      SRJ_CUDA(cudaMemsetAsync(plan.vtb_yh, 0, bytes, st));
+      SRJ_CUDA(cudaMemsetAsync(plan.vtb_yl, 0, bytes, st));
+      vtb_recip<<<sm_count() * 8, 256, 0, st>>>(d.coef_arrays[0] + ioff, plan.vtb_yh + ioff,
+                                                plan.vtb_yl + ioff, l.pitch, int(l.n[0]),
+                                                int(l.n[1]));
+      SRJ_CUDA(cudaGetLastError());
+    }
+    p.yh = plan.vtb_yh + ioff;
+    p.yl = plan.vtb_yl + ioff;
     p.pitch = l.pitch;
     p.n0 = int(l.n[0]);
     p.n1 = int(l.n[1]);
@@ -739,6 +760,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     // last interior column (relative to the row origin) a double2 load may
     // start at: element origin+1+col+1 stays inside the padded row
     p.col_max = int(l.pitch - (l.origin + 1) - 2) & ~1;
+    p.mcol_max = int(l.pitch - (l.origin + 1) - 4) & ~3;
     p.omega[0] = om[0];
     p.omega[1] = om[1];
     p.norms = norms;

@@ -4,13 +4,13 @@
 
 namespace srj_host {
 
-template <bool NL>
+template <bool NL, bool MASK>
 static int vtb_bps() {
   static std::atomic<int> cache[kMaxDevices];
   return cached_per_device(cache, [] {
     int n = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep2d_vtb<NL>, kWarps2DVTB * 32,
-                                                  kVTBSmem);
+                                                  MASK ? kVTBSmemMask : kVTBSmem);
     return n > 0 ? n : 1;
   });
 }
@@ -18,7 +18,11 @@ static int vtb_bps() {
 int launch_var2d_tb(VarTB2DParams p, bool nl, cudaStream_t st) {
   const int rows = p.own_e - p.own_b;
   p.nbands = (p.n1 + kVTBOwn - 1) / kVTBOwn;  // owned columns cover [0, n1)
-  const long capacity = long(sm_count()) * (nl ? vtb_bps<true>() : vtb_bps<false>()) * kWarps2DVTB;
+  const bool mask = p.act != nullptr;
+  const int bps = nl ? (mask ? vtb_bps<true, true>() : vtb_bps<true, false>())
+                     : (mask ? vtb_bps<false, true>() : vtb_bps<false, false>());
+  const long capacity = long(sm_count()) * bps * kWarps2DVTB;
+  const size_t smem = mask ? kVTBSmemMask : kVTBSmem;
   // strips: best fill of whole waves, discounting the 3 fill ticks per strip
   int nstrips = 1;
   double best = -1.0;
@@ -37,9 +41,9 @@ int launch_var2d_tb(VarTB2DParams p, bool nl, cudaStream_t st) {
   const long warps = long(p.nbands) * p.nstrips;
   const int blocks = int((warps + kWarps2DVTB - 1) / kWarps2DVTB);
   if (nl)
-    sweep2d_vtb<true><<<blocks, kWarps2DVTB * 32, kVTBSmem, st>>>(p);
+    sweep2d_vtb<true><<<blocks, kWarps2DVTB * 32, smem, st>>>(p);
   else
-    sweep2d_vtb<false><<<blocks, kWarps2DVTB * 32, kVTBSmem, st>>>(p);
+    sweep2d_vtb<false><<<blocks, kWarps2DVTB * 32, smem, st>>>(p);
   SRJ_CUDA(cudaGetLastError());
   return SRJ_OK;
 }

@@ -21,7 +21,13 @@
 //     and no prefetch lives in registers (the first version prefetched one
 //     row into registers: 164 registers, 12 warps/SM, latency-bound at 86
 //     GLUPS).
-// Division is the IEEE one (the centre varies); dmax and rmax per cell.
+// Division: per-cell double-word reciprocals yh = RN(1/c), yl = RN((1 -
+// c*yh)/c), precomputed once per plan (vtb_recip below, the host formula of
+// the constant-stencil path), feed the 4-op correctly rounded div_recip; cells
+// whose centre is outside [2^-100, 2^100] (yh = 0) or whose numerator is
+// outside div_recip's range take the IEEE division after a warp vote.  (With
+// the IEEE division inline the kernel spent 37% of its instructions in it.)
+// dmax and rmax per cell.
 // Inactive (masked) cells, ghost columns and rows outside [lo_c, hi_c) pass
 // their value through; only owned rows and columns are stored and counted.
 #pragma once
@@ -35,12 +41,14 @@ struct VarTB2DParams {
   const double *f;    // source s, or kappa for the nonlinear source
   const uint8_t *act; // mask (padded byte layout) or nullptr
   const double *c, *am0, *ap0, *am1, *ap1;
+  const double *yh, *yl;  // per-cell double-word reciprocal of c (padded layout)
   int64_t pitch;
   int n0, n1;
   int lo_c, hi_c;     // rows relaxed: [lo_c, hi_c)
   int ld_lo, ld_hi;   // rows present in memory: [ld_lo, ld_hi]
   int own_b, own_e;   // rows stored and counted
   int col_max;        // largest even interior column a double2 load may start at
+  int mcol_max;       // largest 4-aligned interior column a 4-byte mask copy may start at
   int H, nbands, nstrips;
   double omega[2];
   double *norms;      // [2][2]: (dmax, rmax) per step
@@ -48,13 +56,20 @@ struct VarTB2DParams {
 
 constexpr int kWarps2DVTB = 1;   // one warp per CTA: the ring is per warp
 constexpr int kVTBOwn = 60;      // owned columns per band
-constexpr int kVTBArrays = 7;    // u, f, c, am0, ap0, am1, ap1
+constexpr int kVTBArrays = 9;    // u, f, c, am0, ap0, am1, ap1, yh, yl
 constexpr int kVTBRing = 7;      // rows rho-3 .. rho+3
 constexpr int kVTBAhead = 3;     // rows in flight beyond the current one
-constexpr size_t kVTBSmem = size_t(kVTBRing) * kVTBArrays * 32 * 16;  // 25,088 B per warp
+constexpr int kVTBMaskRow = 80;  // mask bytes per ring row: 17 chunks of 4 (68) + pad
+// dynamic shared memory per warp: 32,256 B (7 per SM); with a mask 32,816 B (6)
+constexpr size_t kVTBSmem = size_t(kVTBRing) * kVTBArrays * 32 * 16;
+constexpr size_t kVTBSmemMask = kVTBSmem + size_t(kVTBRing) * kVTBMaskRow;
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_addr(dst)), "l"(src)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() {
@@ -82,31 +97,42 @@ __global__ void __launch_bounds__(kWarps2DVTB * 32)
     const bool in0 = col >= 0 && col < p.n1, in1 = col + 1 >= 0 && col + 1 < p.n1;
     const bool own_l = lane >= 1 && lane <= 30;  // band columns 2..61
     const int64_t pitch = p.pitch;
-    const double *arr[kVTBArrays] = {p.src, p.f, p.c, p.am0, p.ap0, p.am1, p.ap1};
+    const double *arr[kVTBArrays] = {p.src, p.f, p.c, p.am0, p.ap0, p.am1, p.ap1, p.yh, p.yl};
     auto rowc = [&](int r) { return min(max(r, p.ld_lo), p.ld_hi); };
-    auto slot_of = [&](int r) { return (r - i0 + 3 * kVTBRing) % kVTBRing; };  // r >= i0 - 3
-    auto ring = [&](int r, int k) -> double2 {
-      return vtb_ring[(slot_of(r) * kVTBArrays + k) * 32 + lane];
+    // ring slot of row r: (r - i0 + 3) mod 7, advanced incrementally (an
+    // integer modulo per access cost ~20 instructions)
+    auto wrap = [](int x) { return x >= kVTBRing ? x - kVTBRing : x; };
+    auto ring_at = [&](int slot, int k) -> double2 {
+      return vtb_ring[(slot * kVTBArrays + k) * 32 + lane];
     };
-    auto issue = [&](int r) {  // row r of the seven arrays -> its ring slot (one commit group)
-      const int64_t o = int64_t(rowc(r)) * pitch + colc;
-      double2 *dst = vtb_ring + slot_of(r) * kVTBArrays * 32 + lane;
+    // mask bytes of a band row: 17 four-byte chunks from column col0 - 2
+    // (4-byte aligned: the padded rows start 16 B past 64-element boundaries
+    // and col0 = 60 band - 2), lanes 0..16; lane l's cells are bytes 2l+2, 2l+3
+    unsigned char *mring = reinterpret_cast<unsigned char *>(vtb_ring + kVTBRing * kVTBArrays * 32);
+    const int col0 = band * kVTBOwn - 2;
+    const int mcs = min(col0 - 2 + 4 * lane, p.mcol_max);
+    auto issue_slot = [&](int r, int slot) {  // row r -> ring slot (one commit group)
+      const int64_t rb = int64_t(rowc(r)) * pitch;
+      const int64_t o = rb + colc;
+      double2 *dst = vtb_ring + slot * kVTBArrays * 32 + lane;
 #pragma unroll
       for (int k = 0; k < kVTBArrays; ++k) cp_async16(dst + k * 32, arr[k] + o);
+      if (p.act && lane <= 16) cp_async4(mring + slot * kVTBMaskRow + 4 * lane, p.act + rb + mcs);
       cp_async_commit();
     };
-    auto mask2 = [&](int r) -> unsigned {
+    auto mask_at = [&](int slot) -> unsigned {
       if (!p.act) return 3u;
-      const unsigned short m = __ldg(
-          reinterpret_cast<const unsigned short *>(p.act + int64_t(rowc(r)) * pitch + colc));
+      const unsigned short m =
+          *reinterpret_cast<const unsigned short *>(mring + slot * kVTBMaskRow + 2 * lane + 2);
       return (m & 0xffu ? 1u : 0u) | (m >> 8 ? 2u : 0u);
     };
     // one relaxation of the lane's two cells of row r with the coefficients
     // of ring row r: returns the new pair, counts owned cells
-    auto relax_row = [&](int t, int r, const double2 &um, const double2 &uc, const double2 &ud,
-                         unsigned mk) {
-      const double2 f = ring(r, 1), c = ring(r, 2), a0 = ring(r, 3), b0 = ring(r, 4),
-                    a1 = ring(r, 5), b1 = ring(r, 6);
+    auto relax_row = [&](int t, int r, int slot, const double2 &um, const double2 &uc,
+                         const double2 &ud, unsigned mk) {
+      const double2 f = ring_at(slot, 1), c = ring_at(slot, 2), a0 = ring_at(slot, 3),
+                    b0 = ring_at(slot, 4), a1 = ring_at(slot, 5), b1 = ring_at(slot, 6),
+                    yh = ring_at(slot, 7), yl = ring_at(slot, 8);
       const double w = __shfl_up_sync(kFull, uc.y, 1);
       const double e = __shfl_down_sync(kFull, uc.x, 1);
       const bool row_ok = r >= p.lo_c && r < p.hi_c;
@@ -114,42 +140,56 @@ __global__ void __launch_bounds__(kWarps2DVTB * 32)
       const double ucv[2] = {uc.x, uc.y}, umv[2] = {um.x, um.y}, udv[2] = {ud.x, ud.y},
                    fv[2] = {f.x, f.y}, cv[2] = {c.x, c.y}, a0v[2] = {a0.x, a0.y},
                    b0v[2] = {b0.x, b0.y}, a1v[2] = {a1.x, a1.y}, b1v[2] = {b1.x, b1.y},
-                   wv[2] = {w, uc.x}, ev[2] = {uc.y, e};
-      double yv[2];
+                   yhv[2] = {yh.x, yh.y}, ylv[2] = {yl.x, yl.y}, wv[2] = {w, uc.x},
+                   ev[2] = {uc.y, e};
+      double nm[2], d[2], rr[2];
+      bool act[2], slow = false;
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         // lane 0's west / lane 31's east neighbour is outside the band: those
         // two cells are never needed by stage 2 of an owned column
         const bool edge = (v == 0 && lane == 0) || (v == 1 && lane == 31);
-        const bool act = row_ok && !edge && (v == 0 ? in0 : in1) && ((mk >> v) & 1u);
+        act[v] = row_ok && !edge && (v == 0 ? in0 : in1) && ((mk >> v) & 1u);
         const double s = NL ? nl_source(fv[v], ucv[v]) : fv[v];
-        const double rr = resid5(s, cv[v], ucv[v], a0v[v], umv[v], b0v[v], udv[v], a1v[v], wv[v],
-                                 b1v[v], ev[v]);
-        const double d = __ddiv_rn(__dmul_rn(p.omega[t], act ? rr : 0.0), act ? cv[v] : 1.0);
-        yv[v] = act ? __dadd_rn(ucv[v], d) : ucv[v];
-        if (act && cnt) {
-          acc_absmax(rmx[t], rr);
-          acc_absmax(dmx[t], d);
+        rr[v] = resid5(s, cv[v], ucv[v], a0v[v], umv[v], b0v[v], udv[v], a1v[v], wv[v], b1v[v],
+                       ev[v]);
+        nm[v] = __dmul_rn(p.omega[t], rr[v]);
+        d[v] = div_recip(nm[v], cv[v], yhv[v], ylv[v]);
+        slow |= act[v] && (yhv[v] == 0.0 || recip_unsafe(nm[v]));
+      }
+      if (__any_sync(kFull, slow)) {  // rare: IEEE division for the flagged cells
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+          if (act[v] && (yhv[v] == 0.0 || recip_unsafe(nm[v]))) d[v] = div_ieee(nm[v], cv[v]);
+      }
+      double yv[2];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        yv[v] = act[v] ? __dadd_rn(ucv[v], d[v]) : ucv[v];
+        if (act[v] && cnt) {
+          acc_absmax(rmx[t], rr[v]);
+          acc_absmax(dmx[t], d[v]);
         }
       }
       return make_double2(yv[0], yv[1]);
     };
 
-    // prologue: rows i0-3 .. i0+2 in flight (the ring holds i0-3 .. i0+3)
+    // prologue: rows i0-3 .. i0+2 in flight (the ring holds i0-3 .. i0+3);
+    // row i0-3+x lives in slot x
 #pragma unroll 1
-    for (int r = i0 - 3; r < i0 + kVTBAhead; ++r) issue(r);
+    for (int x = 0; x < kVTBAhead + 3; ++x) issue_slot(i0 - 3 + x, x);
+    int s3 = 0;  // slot of row rho-3 (rho-2: s3+1, rho-1: s3+2, rho: s3+3, rho+3: s3+6, mod 7)
     double2 S0 = make_double2(0.0, 0.0), S1 = S0, S2 = S0;  // stage 1 of rows rho-4..rho-2
-    unsigned mk1 = mask2(i0 - 1), mk2 = mask2(i0 - 3);      // masks of rows rho-1, rho-3
     const bool st0 = own_l && in0, st1 = own_l && in1;
 #pragma unroll 1
     for (int rho = i0; rho <= i1 + 2; ++rho) {
-      issue(rho + kVTBAhead);
-      cp_async_wait<kVTBAhead>();  // rows <= rho have landed
-      const unsigned mk1n = mask2(rho), mk2n = mask2(rho - 2);
+      const int s2 = wrap(s3 + 1), s1 = wrap(s3 + 2), s0 = wrap(s3 + 3), sn = wrap(s3 + 6);
+      issue_slot(rho + kVTBAhead, sn);  // row rho+3 into the slot row rho-4 left
+      cp_async_wait<kVTBAhead>();       // rows <= rho have landed
       // stage 2: row rho-3 from stage-1 rows rho-4, rho-3, rho-2
       const int r2 = rho - 3;
       if (r2 >= i0) {
-        const double2 y = relax_row(1, r2, S0, S1, S2, mk2);
+        const double2 y = relax_row(1, r2, s3, S0, S1, S2, mask_at(s3));
         double *out = p.dst + int64_t(r2) * pitch + col;
         if (st0 && st1) {
           *reinterpret_cast<double2 *>(out) = y;
@@ -159,13 +199,12 @@ __global__ void __launch_bounds__(kWarps2DVTB * 32)
         }
       }
       // stage 1: row rho-1 from u rows rho-2, rho-1, rho
-      const double2 s1 = relax_row(0, rho - 1, ring(rho - 2, 0), ring(rho - 1, 0), ring(rho, 0),
-                                   mk1);
+      const double2 y1 = relax_row(0, rho - 1, s1, ring_at(s2, 0), ring_at(s1, 0),
+                                   ring_at(s0, 0), mask_at(s1));
       S0 = S1;
       S1 = S2;
-      S2 = s1;
-      mk1 = mk1n;
-      mk2 = mk2n;
+      S2 = y1;
+      s3 = s2;
     }
     cp_async_wait<0>();
   }
@@ -177,6 +216,23 @@ __global__ void __launch_bounds__(kWarps2DVTB * 32)
       global_max(p.norms + 2 * t, dm);
       global_max(p.norms + 2 * t + 1, rm);
     }
+  }
+}
+
+// Per-cell double-word reciprocal of the centre over the interior (padded
+// layout; the host's recip_or_zero / recip_lo, bit for bit): yh = RN(1/c)
+// for c in [2^-100, 2^100] (else 0 = use the IEEE division), yl = RN((1 -
+// c*yh)/c).
+static __global__ void vtb_recip(const double *c, double *yh, double *yl, int64_t pitch, int n0, int n1) {
+  const int64_t n = int64_t(n0) * n1;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t o = (q / n1) * pitch + q % n1;
+    const double cc = c[o];
+    const bool ok = cc >= 0x1p-100 && cc <= 0x1p+100;
+    const double h = ok ? __ddiv_rn(1.0, cc) : 0.0;
+    yh[o] = h;
+    yl[o] = ok ? __ddiv_rn(__fma_rn(-cc, h, 1.0), cc) : 0.0;
   }
 }
 
