@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SRJ_ABI_VERSION 5
+#define SRJ_ABI_VERSION 6
 
 enum {
     SRJ_OK = 0,
@@ -150,6 +150,24 @@ int srj_plan_destroy(srj_plan *plan);
  * Like a non-FIXED face, it makes every launch a single sweep. */
 int srj_plan_set_post_gather(srj_plan *plan, const int64_t *dst,
                              const int64_t *src, int64_t n);
+
+/* Coefficient array classes (ABI v6).  Per-cell coefficient arrays that are
+ * constant along an axis -- the reference's problem builders broadcast radial
+ * / polar profiles over the grid, e.g. spherical_poisson's center and lower /
+ * upper (problems.py:489-560), and a constant stencil under a mask is
+ * constant along every axis -- are read once per row instead of once per cell
+ * by the 3D per-cell sweep kernel (srj_sweep3d.cuh; the reference's
+ * spherical problem at 512^3: 69 -> 96 G updates/s).  The 2D per-cell kernels
+ * read every cell (measured: no gain).  cls[a] for
+ * coefficient a (order of coef_arrays) is a bit set:
+ *   SRJ_COEF_CONST_AXIS0: value(i, ...) == value(0, ...) for every i;
+ *   SRJ_COEF_CONST_LAST:  value(..., k) == value(..., 0) for every k.
+ * The arrays stay in coef_arrays (padded layout, every cell present), so the
+ * other kernels and the residual kernels read them as before; the caller
+ * guarantees the equalities bit for bit (engine.py detects them), so every
+ * result is unchanged.  All zero (the default) = read every cell. */
+enum { SRJ_COEF_FULL = 0, SRJ_COEF_CONST_AXIS0 = 1, SRJ_COEF_CONST_LAST = 2 };
+int srj_plan_set_coef_classes(srj_plan *plan, const int32_t *cls);
 
 /* Maximum fused-sweep depth (temporal blocking) supported by srj_plan_run. */
 int srj_max_fuse(void);

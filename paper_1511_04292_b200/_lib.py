@@ -20,7 +20,7 @@ SRJ_EINVAL = -1
 SRJ_ECUDA = -2
 SRJ_ENOMEM = -3
 SRJ_EUNSUPPORTED = -4
-ABI_VERSION = 5
+ABI_VERSION = 6
 SLAB_FLAG_WORDS = 8
 
 BC_KINDS = {"fixed": 0, "mirror": 1, "periodic": 2, "face_dirichlet": 3}
@@ -92,6 +92,7 @@ _SIGNATURES = {
     "srj_plan_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "srj_plan_set_post_gather": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
                                                 ctypes.c_void_p, ctypes.c_int64]),
+    "srj_plan_set_coef_classes": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "srj_plan_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p, _c_dp, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,

@@ -89,6 +89,13 @@ struct KVar2D {
   }
 };
 
+// row / plane stride and column multiplier of coefficient array `a` under
+// its class (srj_plan_set_coef_classes)
+static void class_strides(const int32_t *cls, int a, int64_t stride, int64_t &rs, int &cm) {
+  rs = (cls[a] & SRJ_COEF_CONST_AXIS0) ? 0 : stride;
+  cm = (cls[a] & SRJ_COEF_CONST_LAST) ? 0 : 1;
+}
+
 static int launch_var2d(const srj_plan_desc &d, int64_t own_b, int64_t own_e, const double *cur,
                         double *nxt, const double *f, int ld_lo, int ld_hi, double omega,
                         double *norms, cudaStream_t st) {
@@ -215,6 +222,7 @@ struct srj_plan {
   double *row_parts = nullptr;  // 3D per-(i,j)-row residual partials (srj_plan_residual_layers)
   int64_t row_parts_cap = 0;
   double *vtb_yh = nullptr, *vtb_yl = nullptr;  // per-cell reciprocal of c (sweep2d_vtb)
+  int32_t cls[7] = {};  // coefficient classes (srj_plan_set_coef_classes)
   double *bc_scalars;  // [3][2] device copies of the faces' scalar values (fused BCs)
   // small-grid cluster path: per-chunk omegas (device + pinned staging)
   double *d_omegas = nullptr, *h_omegas = nullptr;
@@ -461,6 +469,18 @@ int srj_plan_set_post_gather(srj_plan *p, const int64_t *dst, const int64_t *src
     return cuda_fail(e, "post-gather setup");
   }
   p->g_n = n;
+  return SRJ_OK;
+}
+
+int srj_plan_set_coef_classes(srj_plan *p, const int32_t *cls) {
+  if (!p || !cls) return fail(SRJ_EINVAL, "null argument");
+  const srj_layout_t &l = p->d.layout;  // read by the 3D per-cell kernel (srj_sweep3d.cuh)
+  for (int a = 0; a < 7; ++a)
+    if (cls[a] < 0 || cls[a] > (SRJ_COEF_CONST_AXIS0 | SRJ_COEF_CONST_LAST))
+      return fail(SRJ_EINVAL, "bad coefficient class %d for array %d", int(cls[a]), a);
+  for (int a = 0; a < 7; ++a) {
+    p->cls[a] = (a < 1 + 2 * l.ndim) ? cls[a] : 0;
+  }
   return SRJ_OK;
 }
 
@@ -901,9 +921,12 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     p.dst = nxt + ioff;
     p.f = f + ioff;
     p.act = d.act ? d.act + ioff : nullptr;
+    bool cls = false;
     for (int a = 0; a < 7; ++a) {
       p.coef[a] = var ? d.coef_arrays[a] + ioff : nullptr;
       p.kc[a] = d.coef[a];
+      class_strides(plan.cls, a, l.plane, p.cplane[a], p.ccol[a]);
+      cls |= var && plan.cls[a] != 0;
     }
     p.pitch = l.pitch;
     p.plane = l.plane;
@@ -922,7 +945,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
     p.kinv_lo = recip_lo(d.coef[0], p.kinv);
     const bool recip = !var && p.kinv != 0.0;
-    const Kernel3D k3 = pick3d(var, nl, recip);
+    const Kernel3D k3 = pick3d(var, nl, recip, cls);
     const long per_strip = long(p.njg) * p.nbands;
     const long capacity = long(sm_count()) * k3.blocks_per_sm() * kWarps3D;
     // strips: best fill of whole waves, discounting the 2 halo planes per strip

@@ -132,7 +132,7 @@ struct Kernel3DTB {
   bool persistent; // sweep3d_rs: grid = resident CTAs, equal (tile, plane) shares
 };
 
-Kernel3D pick3d(bool var, bool nl, bool recip);        // srj_k3d.cu
+Kernel3D pick3d(bool var, bool nl, bool recip, bool cls);  // srj_k3d.cu
 Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf);  // srj_k3d.cu
 // fused T = 2 per-cell-coefficient 2D sweep (srj_kvar.cu); sets H/nbands/nstrips
 int launch_var2d_tb(VarTB2DParams p, bool nl, cudaStream_t st);

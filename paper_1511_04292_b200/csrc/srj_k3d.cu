@@ -5,16 +5,16 @@
 
 namespace srj_host {
 
-template <bool VAR, bool NL, bool RECIP>
+template <bool VAR, bool NL, bool RECIP, bool CLS = false>
 struct K3 {
   static void launch(const Sweep3DParams &p, int blocks, cudaStream_t s) {
-    sweep3d<VAR, NL, RECIP><<<blocks, kWarps3D * 32, 0, s>>>(p);
+    sweep3d<VAR, NL, RECIP, CLS><<<blocks, kWarps3D * 32, 0, s>>>(p);
   }
   static int bps() {
     static std::atomic<int> cache[kMaxDevices];
     return cached_per_device(cache, [] {
       int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d<VAR, NL, RECIP>, kWarps3D * 32, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d<VAR, NL, RECIP, CLS>, kWarps3D * 32, 0);
       return n > 0 ? n : 1;
     });
   }
@@ -107,7 +107,8 @@ Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf) {
   }
 }
 
-Kernel3D pick3d(bool var, bool nl, bool recip) {
+Kernel3D pick3d(bool var, bool nl, bool recip, bool cls) {
+  if (var && cls) return nl ? K3<true, true, false, true>::get() : K3<true, false, false, true>::get();
   if (var) return nl ? K3<true, true, false>::get() : K3<true, false, false>::get();
   if (recip) return nl ? K3<false, true, true>::get() : K3<false, false, true>::get();
   return nl ? K3<false, true, false>::get() : K3<false, false, false>::get();

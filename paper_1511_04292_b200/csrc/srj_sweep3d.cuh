@@ -21,6 +21,8 @@ struct Sweep3DParams {
   const double *f;     // source or kappa (nonlinear)
   const uint8_t *act;
   const double *coef[7];  // c, am0, ap0, am1, ap1, am2, ap2 (VAR)
+  int64_t cplane[7];      // CLS: plane stride of each coefficient array, 0 if constant along axis 0
+  int ccol[7];            // CLS: 1, or 0 if constant along axis 2 (read at k = 0)
   double kc[7];           // constant stencil
   double kinv;            // RN(1/kc[0]) when the reciprocal path is used
   double kinv_lo;      // RN(1/c - kinv): low word of the reciprocal
@@ -35,7 +37,11 @@ struct Sweep3DParams {
 constexpr int kWarps3D = 4;
 constexpr int kRows3D = 2;  // J: axis-1 rows per warp
 
-template <bool VAR, bool NL, bool RECIP>
+// CLS (VAR only): coefficient classes (srj_plan_set_coef_classes) -- arrays
+// constant along axis 0 / axis 2 are read at i = 0 / k = 0 (L1 / L2 hits
+// instead of HBM); a separate instantiation so the all-per-cell path keeps
+// its single offset per cell.
+template <bool VAR, bool NL, bool RECIP, bool CLS = false>
 __global__ void __launch_bounds__(kWarps3D * 32)
     sweep3d(const __grid_constant__ Sweep3DParams p) {
   constexpr int V = 2, BAND = 64, J = kRows3D;  // cells per lane, cells per band
@@ -109,8 +115,15 @@ __global__ void __launch_bounds__(kWarps3D * 32)
           if (VAR) {
             const int64_t o = int64_t(min(i, p.hi_c - 1)) * p.plane +
                               int64_t(min(j0 + q, p.n1 - 1)) * p.pitch + col + v;
+            if (CLS) {
+              const int64_t ii = min(i, p.hi_c - 1), oj = int64_t(min(j0 + q, p.n1 - 1)) * p.pitch;
 #pragma unroll
-            for (int a = 0; a < 7; ++a) k[a] = __ldg(p.coef[a] + o);
+              for (int a = 0; a < 7; ++a)
+                k[a] = __ldg(p.coef[a] + ii * p.cplane[a] + oj + (col + v) * p.ccol[a]);
+            } else {
+#pragma unroll
+              for (int a = 0; a < 7; ++a) k[a] = __ldg(p.coef[a] + o);
+            }
             if (p.act) act = act && (__ldg(p.act + o) != 0);
           } else {
 #pragma unroll

@@ -13,13 +13,14 @@ CPU path: constructing a DeviceGrid without a CUDA device raises.
 """
 
 import ctypes
+import os
 import warnings
 
 import numpy as np
 
 from . import _lib
 
-__all__ = ["DeviceGrid", "constant_value", "require_cuda"]
+__all__ = ["DeviceGrid", "coef_class", "constant_value", "require_cuda"]
 
 
 def require_cuda():
@@ -42,6 +43,27 @@ def constant_value(a):
     if bool(np.all(bits == first.view(np.int64)[0])):
         return float(first[0])
     return None
+
+
+def coef_class(a):
+    """``SRJ_COEF_*`` class bits of an interior-shaped coefficient array
+    (``srj_plan_set_coef_classes``, include/srj.h): 1 if every axis-0 slice
+    equals the first, 2 if every value equals the first of its last-axis row,
+    both bit for bit (so reading the representative changes no result).  The
+    reference's problem builders broadcast such profiles over the grid
+    (spherical_poisson, grad_shafranov: problems.py:489-560, :684-689)."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim < 2 or a.size == 0:
+        return 0
+    bits = a.view(np.int64)
+    cls = 0
+    # a cheap test on two slices rejects most varying arrays before the full one
+    if a.shape[0] >= 2 and np.array_equal(bits[1], bits[0]) and bool(np.all(bits == bits[:1])):
+        cls |= 1
+    if (a.shape[-1] >= 2 and np.array_equal(bits[..., 1], bits[..., 0])
+            and bool(np.all(bits == bits[..., :1]))):
+        cls |= 2
+    return cls
 
 
 def _contig(a, dtype):
@@ -144,6 +166,16 @@ class DeviceGrid:
             _lib.check(lib.srj_plan_create(ctypes.byref(desc), ctypes.byref(plan)),
                        "srj_plan_create")
             self.plan = plan
+            self.coef_classes = [0] * 7
+            # coefficient classes: read by the 3D per-cell kernel (include/srj.h)
+            if (not self.constant and nd == 3
+                    and os.environ.get("SRJ_COEF_CLASSES", "1") != "0"):
+                cls = [coef_class(c) for c in coefs] + [0] * (7 - len(coefs))
+                if any(cls):
+                    arr = (ctypes.c_int32 * 7)(*cls)
+                    _lib.check(lib.srj_plan_set_coef_classes(plan, arr),
+                               "srj_plan_set_coef_classes")
+                    self.coef_classes = cls
             if post_gather is not None and len(post_gather[0]):
                 self._set_post_gather(*post_gather)
             self.norms = torch.zeros(2, dtype=torch.float64, device=self.device)

@@ -167,3 +167,22 @@ def test_post_sweep_gather_probe():
                 lambda uu: (_ for _ in ()).throw(RuntimeError("boom"))):
         with pytest.raises(NotImplementedError):
             G.post_sweep_gather(bad, (4, 3))
+
+
+def test_coef_class_detection():
+    """engine.coef_class: SRJ_COEF_* bits, bit for bit (include/srj.h)."""
+    from paper_1511_04292_b200.engine import coef_class
+
+    rng = np.random.default_rng(0)
+    full = rng.random((5, 7))
+    assert coef_class(full) == 0
+    assert coef_class(np.broadcast_to(rng.random(7), (5, 7))) == 1
+    assert coef_class(np.broadcast_to(rng.random((5, 1)), (5, 7))) == 2
+    assert coef_class(np.full((5, 7), 3.0)) == 3
+    assert coef_class(np.full((5, 1), 3.0)) == 1  # a one-column row is not classed
+    z = np.zeros((4, 3))
+    z[2, 1] = -0.0  # -0.0 == 0.0 numerically but not bitwise
+    assert coef_class(z) == 0
+    three = np.broadcast_to(rng.random((4, 1, 1)), (4, 3, 6))
+    assert coef_class(three) == 2
+    assert coef_class(np.broadcast_to(rng.random((1, 3, 1)), (4, 3, 6))) == 3
