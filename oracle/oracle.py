@@ -329,7 +329,7 @@ def gs_sweep(problem, omega):
     rc = lib.oracle_gs(a.ndim, _ptr(a.n, _i64p), _ptr(u), _ptr(a.s), _ptr(a.c), a.lo_p, a.hi_p,
                        _ptr(a.act, _u8p), float(omega), ctypes.byref(dm), ctypes.byref(rm))
     if rc != 0:
-        raise ValueError("oracle GS supports 2- and 3-dimensional grids")
+        raise ValueError("oracle GS supports 1- to 3-dimensional grids")
     return dm.value, rm.value
 
 

@@ -9,7 +9,7 @@
  * What it restates (reference = /root/reference/pkg/src/srj/grids.py):
  *   oracle_wj1/2/3   <- _wj1 (grids.py:331-348), _wj2 (:351-376), _wj3 (:379-408)
  *   oracle_solve     <- _iterate (:602-629) driven as srj_solve (:642-687)
- *   oracle_gs        <- _gs2 (grids.py:426-448), _gs3 (:450-474): in-place
+ *   oracle_gs        <- _gs1 (grids.py:410-424), _gs2 (:426-448), _gs3 (:450-474): in-place
  *                       lexicographic Gauss-Seidel / SOR sweeps
  *   oracle_residual  <- GridProblem.residual_field (:249-266), reduced to
  *                       (sum r^2, max |r|) -- the L2 norm is this project's
@@ -197,7 +197,18 @@ int oracle_gs(int ndim, const int64_t *n, double *u, const double *s,
               const double *const *upper, const uint8_t *act, double omega,
               double *dmax, double *rmax) {
     double dm = 0.0, rm = 0.0;
-    if (ndim == 2) {
+    if (ndim == 1) { /* _gs1, grids.py:410-424 */
+        for (int64_t i = 0; i < n[0]; ++i) {
+            if (act && !act[i]) continue;
+            const double uc = u[i + 1];
+            const double acc = c[i] * uc + lower[0][i] * u[i] + upper[0][i] * u[i + 2];
+            const double r = s[i] - acc;
+            const double d = omega * r / c[i];
+            u[i + 1] = uc + d;
+            upd_max(&dm, d);
+            upd_max(&rm, r);
+        }
+    } else if (ndim == 2) {
         const int64_t n0 = n[0], n1 = n[1], w = n1 + 2;
         for (int64_t i = 0; i < n0; ++i)
             for (int64_t j = 0; j < n1; ++j) {

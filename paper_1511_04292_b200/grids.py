@@ -7,7 +7,7 @@ module's look-alikes: any object with the ``GridProblem`` attributes
 (``u``, ``source``, ``center``, ``lower``, ``upper``, ``bc``, ``mask`` /
 ``_active``, ``post_sweep``) and any cycle with ``weight_sequence``.
 
-GPU scope: 2-D 5-point and 3-D 7-point stencils with
+GPU scope: 1-D, 2-D 5-point and 3-D 7-point stencils with
 every reference boundary rule (FIXED, mirror and face-Dirichlet faces run
 fused multi-sweep kernels; periodic faces run one sweep per launch; a device
 ghost refresh follows every launch),
@@ -15,8 +15,9 @@ constant or per-cell coefficients, optional mask,
 optional nonlinear source, ``post_sweep`` hooks that copy field values (e.g.
 the spherical ``tie_origin``; applied on the device as a gather after every
 sweep, ``post_sweep_gather``), and Gauss-Seidel / SOR as a bitwise GPU
-wavefront (``srj_plan_gs``).  Hooks that compute values and 1-D grids raise
-``NotImplementedError`` -- there is no CPU fallback.
+wavefront (``srj_plan_gs``).  1-D grids (``_wj1``) run as 1 x n 2-D grids
+(``_LineGrid``).  Hooks that compute values raise ``NotImplementedError`` --
+there is no CPU fallback.
 
 Entry points and the reference code they replace:
 
@@ -266,11 +267,45 @@ class ResidualHistory:
 
 
 # --------------------------------------------------------------------- GPU
+class _LineGrid(DeviceGrid):
+    """A 1-D problem (reference kernel ``_wj1``, ``grids.py:331-348``) staged as
+    a 1 x n two-dimensional grid: the line is the grid's single last-axis row,
+    the axis-0 neighbour coefficients are zero and the two extra ghost rows
+    hold zeros, so every product they add is +0.0 and the 5-point residual
+    ``s - ((((c*u + 0) + 0) + am*u[i-1]) + ap*u[i+1])`` equals ``_wj1``'s
+    ``s - ((c*u + am*u[i-1]) + ap*u[i+1])`` in every nonzero value (a zero can
+    differ in sign only, which no later operation of the sweep can turn into
+    a different value)."""
+
+    def download_field(self, idx, host):
+        if host.ndim == 1:
+            tmp = np.empty((3, host.shape[0]))
+            super().download_field(idx, tmp)
+            host[...] = tmp[1]
+            return
+        super().download_field(idx, host)
+
+
+def _lift_line(problem, active, kappa, gather):
+    """Arguments of a ``_LineGrid`` for a 1-D problem."""
+    n = problem.source.shape[0]
+    u = np.zeros((3, n + 2))
+    u[1] = problem.u
+    row = lambda a: None if a is None else np.asarray(a)[None, :]  # noqa: E731
+    zeros = np.zeros((1, n))
+    if gather is not None:
+        gather = tuple(np.asarray(g, dtype=np.int64) + (n + 2) for g in gather)
+    return dict(u=u, source=row(problem.source), center=row(problem.center),
+                lower=(zeros, row(problem.lower[0])), upper=(zeros, row(problem.upper[0])),
+                active=row(active), kappa=row(kappa), bc=((FIXED, FIXED), tuple(problem.bc[0])),
+                post_gather=gather)
+
+
 def _device_grid(problem):
     """Validate the GPU scope and stage the problem on the device."""
     nd = problem.source.ndim
-    if nd not in (2, 3):
-        raise NotImplementedError("the GPU path supports 2- and 3-dimensional grids")
+    if nd not in (1, 2, 3):
+        raise NotImplementedError("the GPU path supports 1-, 2- and 3-dimensional grids")
     for pair in problem.bc:
         for rule in pair:
             if rule.kind not in ("fixed", "mirror", "periodic", "face_dirichlet"):
@@ -282,6 +317,8 @@ def _device_grid(problem):
     if active is None:
         active = getattr(problem, "mask", None)
     kappa = getattr(problem, "source_kappa", None)
+    if nd == 1:
+        return _LineGrid(**_lift_line(problem, active, kappa, gather))
     return DeviceGrid(problem.u, problem.source, problem.center, problem.lower,
                       problem.upper, active=active, kappa=kappa, bc=problem.bc,
                       post_gather=gather)
@@ -389,13 +426,14 @@ def _solve(problem, weights, tol, max_iters, normalise, stop, check_every, fuse,
         raise ValueError(f"unknown stopping rule {stop!r}")
     dev = _device_grid(problem)
     try:
-        backend = GridBackend(dev, problem.source.shape[0])
+        source = np.atleast_2d(problem.source)  # a 1-D line is one axis-0 layer
+        backend = GridBackend(dev, source.shape[0])
         if stop == "residual_l2" and l2_reference is None:
             if getattr(problem, "source_kappa", None) is not None:
                 l2_reference = lambda: l2_from_layers(  # noqa: E731 - residual of u0
                     backend, LocalComm, dev.residual_layers(0))[0]
             else:
-                l2_reference = source_l2(backend, LocalComm, layer_sum_squares(problem.source))
+                l2_reference = source_l2(backend, LocalComm, layer_sum_squares(source))
         hist, converged, diverged, cur = run_solve(
             backend, LocalComm, weights, tol, max_iters, normalise, stop, check_every, fuse,
             chunk, l2_reference, int(np.prod(problem.source.shape)))

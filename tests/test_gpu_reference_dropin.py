@@ -54,6 +54,8 @@ def _cases(rp):
         # post_sweep hook (tie_origin) + MIRROR theta faces; 3D with a periodic phi axis
         ("spherical_poisson(2, 24)", rp.spherical_poisson(2, 24).problem, (6, 32), 1e-10),
         ("spherical_poisson(3, 12)", rp.spherical_poisson(3, 12).problem, (4, 100), 1e-8),
+        # the reference's 1-D problem (_wj1): mask + tie_origin on a line
+        ("spherical_poisson(1, 96)", rp.spherical_poisson(1, 96).problem, (5, 100), 1e-10),
     ]
 
 

@@ -32,8 +32,10 @@ def _face_shape(shape, ax):
 
 def _case(rg, seed):
     rng = np.random.default_rng(7000 + seed)
-    nd = 2 if seed % 3 else 3
-    if nd == 2:
+    nd = 1 if seed >= 60 else 2 if seed % 3 else 3  # seeds 60+: lines (_wj1)
+    if nd == 1:
+        shape = (int(rng.integers(1, 3000)),)
+    elif nd == 2:
         pick = int(rng.integers(0, 3))
         shape = tuple(int(x) for x in (rng.integers(8, 120, 2) if pick == 0 else
                                        rng.integers(300, 700, 2) if pick == 1 else
@@ -87,7 +89,7 @@ class _Cycle:
         self.weight_sequence = np.asarray(w, dtype=float)
 
 
-@pytest.mark.parametrize("seed", range(int(os.environ.get("SRJ_REF_RANDOM_CASES", "60"))))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SRJ_REF_RANDOM_CASES", "72"))))
 def test_reference_random_problem(ref, seed):  # noqa: F811
     rg = ref[0]
     p, w, fuse, chunk, steps = _case(rg, seed)

@@ -113,7 +113,10 @@ def test_oracle_nonlinear_source_restatement():
 
 
 BC_CASES = ["neumann2d", "periodic2d", "facedir3d", "gs_a", "gs_b", "gs_a_solve",
-            "spherical2d", "spherical3d"]
+            "spherical2d", "spherical3d",
+            # 1-D grids (_wj1, grids.py:331-348; tools/make_golden_1d.py)
+            "line_spherical", "line_var_faces", "line_var_periodic", "line_var_fixed",
+            "line_const_solve"]
 
 
 @pytest.mark.parametrize("name", BC_CASES)
@@ -155,7 +158,8 @@ def test_dependency_cone_crops(name, shape, k):
     assert nd == len(win)
 
 
-GS_CASES = ["gs_var2d", "sor_var2d", "gs_var3d", "sor_var3d", "gs_const2d_solve", "sor_neumann2d"]
+GS_CASES = ["gs_var2d", "sor_var2d", "gs_var3d", "sor_var3d", "gs_const2d_solve", "sor_neumann2d",
+            "gs_line", "sor_line"]
 
 
 @pytest.mark.parametrize("name", GS_CASES)
