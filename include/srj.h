@@ -283,9 +283,12 @@ srj_plan *srj_slab_plan(srj_slab *slab);
  * `src` (0..2, left untouched) ping-ponging over the other two; *final_buf =
  * the buffer index holding the result.  d_norms[i]: device, 2*nsteps doubles
  * of per-step (dmax, rmax) over slab i's owned rows (MAX over ranks is the
- * caller's all-reduce).  n > 1 slabs in one call = ranks emulated on one
- * device, all enqueued on streams[0] in dependency order; n == 1: this
- * process's rank on streams[0] (+ an internal comm stream). */
+ * caller's all-reduce).  n == 1: this process's rank on streams[0] (+ an
+ * internal comm stream).  n > 1 slabs in one call = ranks emulated on one
+ * device: with one shared stream everything is enqueued on it in dependency
+ * order; with pairwise distinct streams[i] every slab runs as a rank would
+ * (its stream + its comm stream, ordered against the others only by the
+ * flag words). */
 int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src,
                  const double *weights, int64_t m, int64_t first, int64_t nsteps,
                  int32_t fuse, double *const *d_norms, int32_t *final_buf,

@@ -1425,10 +1425,14 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
   if (nsteps < 0 || first < 0) return fail(SRJ_EINVAL, "negative step range");
   *final_buf = src;
   if (nsteps == 0) return SRJ_OK;
-  // several slabs in one call (ranks emulated on one device): everything is
-  // enqueued on the one stream in dependency order, so every flag wait is
-  // already satisfied when the stream reaches it
-  const bool serial = n > 1;
+  // several slabs in one call (ranks emulated on one device) that share one
+  // stream: everything is enqueued on it in dependency order, so every flag
+  // wait is already satisfied when the stream reaches it.  Slabs with
+  // distinct streams run exactly as separate ranks do (own stream + comm
+  // stream each, ordered only by the flag words).
+  bool serial = n > 1;
+  for (int i = 1; i < n; ++i)
+    if (streams[i] != streams[0]) serial = false;
   int T = kMaxFuse;
   for (int i = 0; i < n; ++i) {
     srj_slab *sl = slabs[i];

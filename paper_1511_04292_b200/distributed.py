@@ -376,15 +376,29 @@ def run_slabs(slabs, src, weights, first, n, fuse=0):
 class EmulatedRanks:
     """``world`` ranks of a slab decomposition on ONE device in one process,
     exchanging through the same C path (``srj_slab_run`` with all slabs, one
-    stream); the backend interface of ``solver.run_solve`` with the rank
-    combination done here (use ``solver.LocalComm``)."""
+    stream; ``concurrent=True``: one stream per rank, so the flag protocol
+    orders truly asynchronous ranks); the backend interface of
+    ``solver.run_solve`` with the rank combination done here (use
+    ``solver.LocalComm``)."""
 
-    def __init__(self, problem, world, fuse=0, device=None):
+    def __init__(self, problem, world, fuse=0, device=None, concurrent=False):
         nd = problem.source.ndim
         halo = default_halo(nd, fuse)
         n0 = problem.source.shape[0]
         self.decomps = [SlabDecomposition(n0, world, r, halo) for r in range(world)]
-        self.slabs = [DeviceSlab(SlabProblem.from_global(problem, d), device) for d in self.decomps]
+        self.concurrent = bool(concurrent)
+        if concurrent:
+            # one stream per emulated rank: launches, peer copies and flag
+            # operations of different ranks race exactly as between processes
+            import torch
+
+            self.slabs = []
+            for d in self.decomps:
+                with torch.cuda.stream(torch.cuda.Stream(device)):
+                    self.slabs.append(DeviceSlab(SlabProblem.from_global(problem, d), device))
+        else:
+            self.slabs = [DeviceSlab(SlabProblem.from_global(problem, d), device)
+                          for d in self.decomps]
         for r, s in enumerate(self.slabs):
             s.connect_local(self.slabs[r - 1] if r > 0 else None,
                             self.slabs[r + 1] if r + 1 < world else None)
@@ -397,16 +411,35 @@ class EmulatedRanks:
     def run_chunk(self, src, weights, first, n, fuse=0):
         return run_slabs(self.slabs, src, weights, first, n, fuse)
 
+    def _sync(self):
+        if self.concurrent:
+            for s in self.slabs:
+                s.stream.synchronize()
+
+    def _each(self, fn):
+        """fn(slab) per rank, on that rank's stream (device reads included)."""
+        if not self.concurrent:
+            return [fn(s) for s in self.slabs]
+        import torch
+
+        self._sync()
+        out = []
+        for s in self.slabs:
+            with torch.cuda.stream(s.stream):
+                out.append(fn(s))
+        return out
+
     def norms(self, n):
-        return np.max([s.norms(n) for s in self.slabs], axis=0)
+        return np.max(self._each(lambda s: s.norms(n)), axis=0)
 
     def residual_layers(self, buf):
-        return np.concatenate([s.residual_layers(buf) for s in self.slabs])
+        return np.concatenate(self._each(lambda s: s.residual_layers(buf)))
 
     def download_owned(self, buf):
-        return np.concatenate([s.download_owned(buf) for s in self.slabs])
+        return np.concatenate(self._each(lambda s: s.download_owned(buf)))
 
     def close(self):
+        self._sync()
         for s in self.slabs:
             s.close()
 
