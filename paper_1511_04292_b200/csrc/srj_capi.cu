@@ -66,6 +66,20 @@ int waves_2d() {
   return w;
 }
 
+// SRJ_SLAB_SPLIT=0: slab ranks run edge and inner rows on one stream (A/B knob)
+// (read on every srj_slab_run call, so a probe can toggle it in-process)
+bool slab_split_enabled() {
+  const char *e = getenv("SRJ_SLAB_SPLIT");
+  return !(e && *e && atoi(e) == 0);
+}
+
+// SRJ_SLAB_DIRECT=0: slab ranks exchange by edge launches + peer copies
+// instead of storing edge rows from the sweep kernel (A/B knob)
+bool slab_direct_enabled() {
+  const char *e = getenv("SRJ_SLAB_DIRECT");
+  return !(e && *e && atoi(e) == 0);
+}
+
 // SRJ_BPS=<n>: size the 2D grid for n resident blocks per SM (tuning knob)
 int bps_override() {
   static int b = -1;
@@ -729,12 +743,26 @@ static int run_cluster2d(srj_plan &plan, const double *src, double *dst, const d
 // plan's own range, or a part of it: the slab exchange's edge / inner
 // launches).  Per-step (dmax, rmax) are folded into norms[2*q..] with
 // atomicMax, so several parts of one step may share a norm slot.
+// Which launches can store slab edge rows straight into the neighbours' halos
+// (PeerSend): the constant-stencil 2D band kernel at any depth, and in 3D the
+// register-streaming T = 2 kernel plus the one-sweep kernel for a chunk's odd
+// last step.
+static bool direct_send_ok(const srj_plan &plan, int T) {
+  const srj_plan_desc &d = plan.d;
+  if (d.coef_mode != 0 || plan.has_bc) return false;
+  if (d.layout.ndim == 2) return true;
+  return T <= 2 && !rs3d_disabled();
+}
+
 static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const double *cur,
-                        double *nxt, const double *om, int t, double *norms, cudaStream_t st) {
+                        double *nxt, const double *om, int t, double *norms, cudaStream_t st,
+                        const PeerSend *send = nullptr) {
   const srj_plan_desc &d = plan.d;
   const srj_layout_t &l = d.layout;
   const int64_t ioff = interior_offset(l);
   const bool var = d.coef_mode == 1;
+  if (send && (var || !direct_send_ok(plan, t)))
+    return fail(SRJ_EINVAL, "direct halo stores are not available for this launch");
   const bool nl = d.kappa != nullptr;
   const double *f = nl ? d.kappa : d.source;
   int lo_c, hi_c, ld_lo, ld_hi;
@@ -815,6 +843,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     p.ld_hi = ld_hi;
     p.own_b = int(own_b);
     p.own_e = int(own_e);
+    if (send) p.send = *send;
     int bcf = 0;
     if (plan.has_bc && t > 1) {
       bcf = 2;
@@ -872,6 +901,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     p.tma_row0 = l.halo0 * p.rows_per_plane + 1;  // row of (i=0, j=0)
     for (int q = 0; q < t; ++q) p.omega[q] = om[q];
     p.norms = norms;
+    if (send) p.send = *send;
     for (int a = 0; a < 3; ++a)
       for (int side = 0; side < 2; ++side) {
         const srj_face_rule &b = d.bc[a][side];
@@ -888,6 +918,8 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
           if (d.bc[a][side].kind == SRJ_BC_FACE_DIRICHLET) bcf = 1;
     }
     const Kernel3DTB k3 = pick3d_tb(t, nl, p.kinv != 0.0, bcf);
+    if (send && !k3.persistent)
+      return fail(SRJ_EINVAL, "direct halo stores need the register-streaming 3D kernel");
     p.ntj = int((l.n[1] + k3.tj - 1) / k3.tj);
     p.ntk = int((l.n[2] + k3.tk - 1) / k3.tk);
     const long tiles = long(p.ntj) * p.ntk;
@@ -940,6 +972,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     p.ld_hi = ld_hi;
     p.own_b = int(own_b);
     p.own_e = int(own_e);
+    if (send) p.send = *send;
     p.nbands = int((l.n[2] + 63) / 64);
     p.njg = int((l.n[1] + kRows3D - 1) / kRows3D);
     p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
@@ -1029,8 +1062,8 @@ struct srj_slab {
   srj_slab_peer peer[2] = {};
   uint32_t epoch = 0;         // launches run since the last reset (all ranks agree)
   int device = 0;
-  cudaStream_t comm = nullptr;
-  cudaEvent_t ev_edge = nullptr, ev_copy = nullptr;
+  cudaStream_t comm = nullptr, edge = nullptr;  // peer copies; edge-row launches
+  cudaEvent_t ev_edge = nullptr, ev_copy = nullptr, ev_inner = nullptr;
   // local interior row ranges: edges (sent after every launch) and inner
   int64_t part_b[3] = {}, part_e[3] = {};  // [0] lower edge, [1] upper edge, [2] inner (empty: b == e)
 };
@@ -1375,8 +1408,10 @@ int srj_slab_create(const srj_plan_desc *desc, int32_t halo, double *const *bufs
     sl->part_e[2] = b;
   }
   cudaError_t e = cudaStreamCreateWithFlags(&sl->comm, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl->edge, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl->ev_edge, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl->ev_copy, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl->ev_inner, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     srj_slab_destroy(sl);
     return cuda_fail(e, "slab stream/event creation");
@@ -1406,8 +1441,10 @@ int srj_slab_reset(srj_slab *sl, void *stream) {
 int srj_slab_destroy(srj_slab *sl) {
   if (!sl) return SRJ_OK;
   if (sl->comm) cudaStreamDestroy(sl->comm);
+  if (sl->edge) cudaStreamDestroy(sl->edge);
   if (sl->ev_edge) cudaEventDestroy(sl->ev_edge);
   if (sl->ev_copy) cudaEventDestroy(sl->ev_copy);
+  if (sl->ev_inner) cudaEventDestroy(sl->ev_inner);
   if (sl->plan) srj_plan_destroy(sl->plan);
   delete sl;
   return SRJ_OK;
@@ -1445,6 +1482,86 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
                              static_cast<cudaStream_t>(streams[serial ? 0 : i])));
   }
   const int others[3][2] = {{1, 2}, {0, 2}, {0, 1}};
+  // Direct mode (default where every launch of the run supports it): ONE
+  // launch per fused step over all owned rows; the sweep kernel stores the
+  // edge rows into the neighbours' halo rows of the destination buffer as it
+  // produces them (PeerSend, peer memory over NVLink), and two flag writes
+  // follow the kernel.  Per launch: wait "halo of my source delivered" and
+  // "neighbour finished the launch that read the buffer I write into", the
+  // kernel, then "my rows arrived" + "I finished this launch".
+  bool direct = slab_direct_enabled();
+  for (int i = 0; i < n; ++i) direct = direct && direct_send_ok(*slabs[i]->plan, T);
+  if (direct) {
+    int cur = src, flip = 0;
+    for (int64_t k = 0; k < nsteps;) {
+      const int t = int(std::min<int64_t>(T, nsteps - k));
+      const int dst = others[src][flip];
+      double om[kMaxFuse];
+      for (int q = 0; q < t; ++q) om[q] = weights[(first + k + q) % m];
+      for (int i = 0; i < n; ++i) {
+        srj_slab *sl = slabs[i];
+        cudaStream_t st = static_cast<cudaStream_t>(streams[serial ? 0 : i]);
+        const srj_plan_desc &d = sl->plan->d;
+        const int64_t ioff = interior_offset(d.layout);
+        FlagOps ops;
+        PeerSend ps;
+        for (int sd = 0; sd < 2; ++sd) {
+          if (!sl->has[sd]) continue;
+          ops.wait(sl->flags + kFlagArrived + sd, sl->epoch);
+          ops.wait(sl->flags + kFlagDone + sd, sl->epoch);
+          const srj_slab_peer &pr = sl->peer[sd];
+          if (sd == 0) {
+            ps.lo = pr.bufs[dst] + ioff;
+            ps.lo_end = int(d.own0_begin) + sl->halo;
+            ps.lo_shift = int(pr.dst_row - d.own0_begin);
+          } else {
+            ps.hi = pr.bufs[dst] + ioff;
+            ps.hi_beg = int(d.own0_end) - sl->halo;
+            ps.hi_shift = int(pr.dst_row - (d.own0_end - sl->halo));
+          }
+        }
+        int rc = ops.flush(st);
+        if (rc != SRJ_OK) return rc;
+        rc = launch_fused(*sl->plan, d.own0_begin, d.own0_end, sl->bufs[cur], sl->bufs[dst], om, t,
+                          d_norms[i] + 2 * k, st, (sl->has[0] || sl->has[1]) ? &ps : nullptr);
+        if (rc != SRJ_OK) return rc;
+        for (int sd = 0; sd < 2; ++sd) {
+          if (!sl->has[sd]) continue;
+          // the neighbour sees this rank on its opposite side
+          ops.write(sl->peer[sd].flags + kFlagArrived + (1 - sd), sl->epoch + 1);
+          ops.write(sl->peer[sd].flags + kFlagDone + (1 - sd), sl->epoch + 1);
+        }
+        rc = ops.flush(st);
+        if (rc != SRJ_OK) return rc;
+        sl->epoch += 1;
+      }
+      k += t;
+      cur = dst;
+      flip ^= 1;
+    }
+    *final_buf = cur;
+    return SRJ_OK;
+  }
+  // A rank with neighbours (not serial) runs on three streams: its edge-row
+  // launches on sl->edge, the peer copies on sl->comm and the inner-row
+  // launches on the caller's stream.  The inner rows of launch j read no halo
+  // row, so they run concurrently with launch j's edge rows; the two streams
+  // meet once per launch (each waits for the other's previous launch, whose
+  // rows its dependency cone reads and whose source rows it overwrites).
+  // (SRJ_SLAB_SPLIT=0: edge and inner rows back to back on one stream.)
+  const bool split_on = slab_split_enabled();
+  auto split = [&](const srj_slab *sl) {
+    return split_on && !serial && (sl->has[0] || sl->has[1]);
+  };
+  for (int i = 0; i < n; ++i) {
+    srj_slab *sl = slabs[i];
+    if (!split(sl)) continue;
+    // the edge stream starts after everything queued on the caller's stream
+    // (the norm memset above, the previous chunk, uploads)
+    cudaStream_t st = static_cast<cudaStream_t>(streams[i]);
+    SRJ_CUDA(cudaEventRecord(sl->ev_inner, st));
+    SRJ_CUDA(cudaStreamWaitEvent(sl->edge, sl->ev_inner, 0));
+  }
   int cur = src, flip = 0;
   int64_t k = 0;
   while (k < nsteps) {
@@ -1456,18 +1573,26 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
     for (int i = 0; i < n; ++i) {
       srj_slab *sl = slabs[i];
       cudaStream_t st = static_cast<cudaStream_t>(streams[serial ? 0 : i]);
+      cudaStream_t es = split(sl) ? sl->edge : st;
       FlagOps ops;
       for (int sd = 0; sd < 2; ++sd)
         if (sl->has[sd]) ops.wait(sl->flags + kFlagArrived + sd, sl->epoch);
-      int rc = ops.flush(st);
+      int rc = ops.flush(es);
       if (rc != SRJ_OK) return rc;
+      if (split(sl) && k > 0) {
+        // the previous launch's inner rows (read by this cone, and the last
+        // readers of the rows written now) and its peer copy (reads the
+        // buffer the launch after this one overwrites)
+        SRJ_CUDA(cudaStreamWaitEvent(es, sl->ev_inner, 0));
+        SRJ_CUDA(cudaStreamWaitEvent(es, sl->ev_copy, 0));
+      }
       for (int part = 0; part < 2; ++part)
         if (sl->part_e[part] > sl->part_b[part]) {
           rc = launch_fused(*sl->plan, sl->part_b[part], sl->part_e[part], sl->bufs[cur],
-                            sl->bufs[dst], om, t, d_norms[i] + 2 * k, st);
+                            sl->bufs[dst], om, t, d_norms[i] + 2 * k, es);
           if (rc != SRJ_OK) return rc;
         }
-      if (!serial) SRJ_CUDA(cudaEventRecord(sl->ev_edge, st));
+      if (!serial) SRJ_CUDA(cudaEventRecord(sl->ev_edge, es));
     }
     // phase B: send the edge rows into the neighbours' halo rows of `dst`
     // once they finished every launch that read that buffer
@@ -1496,29 +1621,46 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
       if (rc != SRJ_OK) return rc;
       if (!serial) SRJ_CUDA(cudaEventRecord(sl->ev_copy, cs));
     }
-    // phase C: inner rows while the halo rows travel; then tell the
-    // neighbours this launch (and its reads of `cur`) is complete
+    // phase C: inner rows (concurrent with this launch's edge rows and
+    // their transfer); then tell the neighbours this launch (and its reads
+    // of `cur`) is complete
     for (int i = 0; i < n; ++i) {
       srj_slab *sl = slabs[i];
       cudaStream_t st = static_cast<cudaStream_t>(streams[serial ? 0 : i]);
+      // first launch of a call: one-time set-up inside launch_fused (e.g. the
+      // reciprocal arrays of the fused per-cell kernel) is queued on the edge
+      // stream, so the inner rows follow it
+      if (split(sl) && k == 0) SRJ_CUDA(cudaStreamWaitEvent(st, sl->ev_edge, 0));
       if (sl->part_e[2] > sl->part_b[2]) {
         const int rc = launch_fused(*sl->plan, sl->part_b[2], sl->part_e[2], sl->bufs[cur],
                                     sl->bufs[dst], om, t, d_norms[i] + 2 * k, st);
         if (rc != SRJ_OK) return rc;
+      }
+      if (split(sl)) {
+        SRJ_CUDA(cudaEventRecord(sl->ev_inner, st));
+        SRJ_CUDA(cudaStreamWaitEvent(st, sl->ev_edge, 0));  // launch complete = both parts
       }
       FlagOps ops;
       for (int sd = 0; sd < 2; ++sd)
         if (sl->has[sd]) ops.write(sl->peer[sd].flags + kFlagDone + (1 - sd), sl->epoch + 1);
       const int rc = ops.flush(st);
       if (rc != SRJ_OK) return rc;
-      // the next launches overwrite rows the copy of this one reads
-      if (!serial && (sl->has[0] || sl->has[1])) SRJ_CUDA(cudaStreamWaitEvent(st, sl->ev_copy, 0));
+      // one stream for both parts: the next launches overwrite rows the
+      // copy of this one reads
+      if (!serial && !split(sl) && (sl->has[0] || sl->has[1]))
+        SRJ_CUDA(cudaStreamWaitEvent(st, sl->ev_copy, 0));
       sl->epoch += 1;
     }
     k += t;
     cur = dst;
     flip ^= 1;
   }
+  // the caller's stream ends behind the last peer copy: whatever it runs next
+  // (the norm all-reduce, which every rank joins only after this point, a
+  // residual pass, the next chunk) sees every halo row delivered by THIS rank
+  for (int i = 0; i < n; ++i)
+    if (split(slabs[i]))
+      SRJ_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(streams[i]), slabs[i]->ev_copy, 0));
   *final_buf = cur;
   return SRJ_OK;
 }

@@ -15,6 +15,20 @@ namespace srj {
 constexpr int kMaxFuse = 8;       // deepest temporal blocking supported
 constexpr unsigned kFull = 0xffffffffu;
 
+// Direct halo stores of a slab rank (srj_slab_run): the sweep kernel writes
+// the axis-0 rows / planes it owns next to a neighbour rank ALSO into that
+// neighbour's halo rows of the destination buffer -- peer memory over NVLink
+// (CUDA IPC mapping) -- so the exchange is part of the sweep itself: no edge
+// launches, no copies, one flag write after the kernel.  Rows [own_b, lo_end)
+// land `lo_shift` rows away in `lo`, rows [hi_beg, own_e) `hi_shift` rows away
+// in `hi` (both the neighbour buffers' interior origins, same pitch / plane).
+// No neighbour: lo_end = INT_MIN / hi_beg = INT_MAX, so the tests never pass.
+struct PeerSend {
+  double *lo = nullptr, *hi = nullptr;
+  int lo_end = -2147483647 - 1, hi_beg = 2147483647;
+  int lo_shift = 0, hi_shift = 0;
+};
+
 // Nonlinear source s(psi) = kappa * psi^5, fixed order:
 //   p2 = psi*psi ; p4 = p2*p2 ; s = kappa * (p4*psi)
 __device__ __forceinline__ double nl_source(double kappa, double psi) {

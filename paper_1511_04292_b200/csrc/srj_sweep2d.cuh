@@ -65,6 +65,7 @@ struct Sweep2DParams {
   int bc_kind[2][2];           // SRJ_BC_* per (axis, side)
   const double *bc_ptr[2][2];  // face_dirichlet value at face position q: bc_ptr[q * bc_step]
   int bc_step[2][2];           // 1: per-position array; 0: the face's scalar
+  PeerSend send;               // slab ranks: rows also stored into the neighbours' halos
 };
 
 template <int T, int V_ = 2>
@@ -433,17 +434,25 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
       }
       const int rs = rho - 2 * T;  // yT holds stage-T row rs
       if (rs >= i0 && rs < i1) {
-        if (lane_owned) {
+        auto store_row = [&](double *o) {
+          if (lane_owned) {
 #pragma unroll
-          for (int v = 0; v < V; v += 2)
-            *reinterpret_cast<double2 *>(out + v) = make_double2(yT[v], yT[v + 1]);
-        } else {
+            for (int v = 0; v < V; v += 2)
+              *reinterpret_cast<double2 *>(o + v) = make_double2(yT[v], yT[v + 1]);
+          } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const int col = lane_col + v;
-            if (col >= own_c0 && col < own_c1) out[v] = yT[v];
+            for (int v = 0; v < V; ++v) {
+              const int col = lane_col + v;
+              if (col >= own_c0 && col < own_c1) o[v] = yT[v];
+            }
           }
-        }
+        };
+        store_row(out);
+        // slab edge rows: the same cells into the neighbour's halo row
+        if (rs < p.send.lo_end)
+          store_row(p.send.lo + int64_t(rs + p.send.lo_shift) * p.pitch + lane_col);
+        if (rs >= p.send.hi_beg)
+          store_row(p.send.hi + int64_t(rs + p.send.hi_shift) * p.pitch + lane_col);
       }
       out += p.pitch;
     }

@@ -32,6 +32,7 @@ struct Sweep3DParams {
   int H, nbands, nstrips, njg;
   double omega;
   double *norms;          // [2]
+  PeerSend send;          // slab ranks: planes also stored into the neighbours' halos
 };
 
 constexpr int kWarps3D = 4;
@@ -163,12 +164,20 @@ __global__ void __launch_bounds__(kWarps3D * 32)
 #pragma unroll
       for (int q = 0; q < J; ++q) {
         if (j0 + q < p.n1) {
-          double *o = out + int64_t(q) * p.pitch;
-          if (in0 && in1) {
-            *reinterpret_cast<double2 *>(o) = make_double2(y[q][0], y[q][1]);
-          } else if (in0) {
-            o[0] = y[q][0];
-          }
+          auto store_row = [&](double *o) {
+            if (in0 && in1) {
+              *reinterpret_cast<double2 *>(o) = make_double2(y[q][0], y[q][1]);
+            } else if (in0) {
+              o[0] = y[q][0];
+            }
+          };
+          store_row(out + int64_t(q) * p.pitch);
+          // slab edge planes: the same cells into the neighbour's halo plane
+          const int64_t inplane = int64_t(j0 + q) * p.pitch + col;
+          if (i < p.send.lo_end)
+            store_row(p.send.lo + int64_t(i + p.send.lo_shift) * p.plane + inplane);
+          if (i >= p.send.hi_beg)
+            store_row(p.send.hi + int64_t(i + p.send.hi_shift) * p.plane + inplane);
         }
         um[q] = uc[q];
         uc[q] = ud[q];

@@ -275,6 +275,21 @@ __global__ void __launch_bounds__(RS3D::THREADS, 2)
 
     const bool bad2 = stage2(std::false_type{});
     if (RECIP && __any_sync(kFull, bad2)) stage2(std::true_type{});
+    // slab edge planes (a few per launch): every thread copies the cells it
+    // just stored into the neighbour's halo plane -- outside the stage code,
+    // so the hot path keeps its registers and instruction count
+    if (po2 && (pl2 < p.send.lo_end || pl2 >= p.send.hi_beg)) {
+      auto send_plane = [&](double *peer, int shift) {
+        double *rrow = peer + int64_t(pl2 + shift) * p.plane + g0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int64_t o = (c >> 1) * p.pitch + 32 * (c & 1);
+          if (pa2 && ((act2 >> c) & 1u)) rrow[o] = drow[o];
+        }
+      };
+      if (pl2 < p.send.lo_end) send_plane(p.send.lo, p.send.lo_shift);
+      if (pl2 >= p.send.hi_beg) send_plane(p.send.hi, p.send.hi_shift);
+    }
     const bool bad1 = stage1(std::false_type{});
     if (RECIP && __any_sync(kFull, bad1)) stage1(std::true_type{});
     __syncthreads();

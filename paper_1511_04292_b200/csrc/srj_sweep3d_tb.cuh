@@ -48,6 +48,7 @@ struct Sweep3DTBParams {
   int bc_kind[3][2];           // SRJ_BC_* per (axis, side)
   const double *bc_ptr[3][2];  // face_dirichlet value at face position q: bc_ptr[q * bc_step]
   int bc_step[3][2];           // 1: per-position array; 0: the face's scalar
+  PeerSend send;               // slab ranks (sweep3d_rs): planes also stored into the neighbours' halos
 };
 
 // The refreshed ghost next to boundary cell value adj at face position q
