@@ -610,6 +610,11 @@ def run_gpu(args):
     cpu, cpu_port = None, None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu, cpu_port = cpu_baselines(args.workload)  # before CUDA initialises
+    if ws > 1:
+        # every stream of a rank on its own hardware queue: the slab exchange's
+        # flag waits must never sit ahead of another stream's work in a shared
+        # queue (read when the CUDA context is created)
+        os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     torch.cuda.set_device(local)
     comm = None
     if ws > 1:
@@ -634,7 +639,9 @@ def run_gpu(args):
     if nd == 3:
         T = min(T, 2 if not args.fuse else args.fuse)
     fused_per_step = -(-sweeps // T)
-    parts = launches_per_fused_step(host) if ws > 1 else 1
+    parts = 1
+    if ws > 1 and not grid.backend.direct(args.fuse):
+        parts = launches_per_fused_step(host)  # staged path: edge parts + inner part
 
     def one_step(cur, first):
         out = grid.run(cur, w, first, sweeps, args.fuse)
@@ -691,9 +698,13 @@ def run_gpu(args):
         comm.barrier()
     if rank != 0:
         return 0
+    if ws > 1:
+        how = ("edge rows stored into the neighbours' halos by the sweep kernel (CUDA IPC peer "
+               "memory over NVLink)" if parts == 1 else
+               "edge launches + peer copies over CUDA IPC / NVLink overlapped with the inner rows")
     par = "single GPU" if ws == 1 else (
-        f"{'row blocks' if nd == 2 else 'z-slabs'} x{ws} (axis 0), halo {T}, C exchange over "
-        f"CUDA IPC + NVLink peer copies, NCCL all-reduce per chunk")
+        f"{'row blocks' if nd == 2 else 'z-slabs'} x{ws} (axis 0), halo {T}, {how}, device-side "
+        f"flag ordering, NCCL all-reduce per chunk")
     line = {
         "metric": METRIC, "value": value, "unit": "GLUPS", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True,

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SRJ_ABI_VERSION 6
+#define SRJ_ABI_VERSION 7
 
 enum {
     SRJ_OK = 0,
@@ -243,13 +243,19 @@ int srj_copy_layers(const srj_layout_t *lay, const double *src,
  * the global grid plus `halo` >= fuse exchanged rows per neighbour side, held
  * as interior rows of its local plan (desc.own0_begin/end = the owned rows).
  * srj_slab_run replaces the per-step loop of _iterate/_Sweeper.jacobi
- * (grids.py:613-617, :544-559) for one rank: per fused launch it relaxes the
- * edge rows, copies them into the neighbours' halo rows of the destination
- * buffer over NVLink (peer cudaMemcpyAsync on a side stream), and relaxes the
- * inner rows meanwhile.  Ranks order each other on the device through flag
- * words in each other's memory (stream memory operations: wait for "halo of
- * my source delivered" before the edge launch, "neighbour finished reading
- * the buffer I write into" before the copy), so the host only enqueues work.
+ * (grids.py:613-617, :544-559) for one rank.  Ranks order each other on the
+ * device through flag words in each other's memory (stream memory operations:
+ * "halo of my source delivered", "neighbour finished the launch that read the
+ * buffer I write into"), so the host only enqueues work.  Two data paths:
+ *  - direct (default; constant stencil, 2D fused depth <= 4, 3D depth <= 2):
+ *    ONE launch per fused step over all owned rows; the sweep kernel itself
+ *    stores the rows next to a neighbour into that neighbour's halo rows of
+ *    the destination buffer (peer memory over NVLink) -- no edge launches, no
+ *    copies, one batch of flag operations per launch;
+ *  - staged (per-cell coefficients, deeper fusion; SRJ_SLAB_DIRECT=0): the
+ *    edge rows run on an internal edge stream, are copied into the
+ *    neighbours' halo rows (peer cudaMemcpyAsync on a comm stream) while the
+ *    inner rows run concurrently on the caller's stream.
  * ------------------------------------------------------------------------ */
 #define SRJ_SLAB_FLAG_WORDS 8   /* uint32 flag words per rank (device)       */
 
@@ -279,6 +285,10 @@ int srj_slab_reset(srj_slab *slab, void *stream);
 int srj_slab_destroy(srj_slab *slab);
 /* The slab's plan (for srj_plan_residual_layers etc.; owned by the slab). */
 srj_plan *srj_slab_plan(srj_slab *slab);
+/* 1 if srj_slab_run with this `fuse` takes the direct data path (one launch
+ * per fused step, edge rows stored into the neighbours' halos by the sweep
+ * kernel), 0 for the staged path (edge launches + peer copies), < 0 on error. */
+int srj_slab_direct(srj_slab *slab, int32_t fuse);
 /* Steps first .. first+nsteps-1 (omega_k = weights[k mod m]) from field buffer
  * `src` (0..2, left untouched) ping-ponging over the other two; *final_buf =
  * the buffer index holding the result.  d_norms[i]: device, 2*nsteps doubles

@@ -20,7 +20,7 @@ SRJ_EINVAL = -1
 SRJ_ECUDA = -2
 SRJ_ENOMEM = -3
 SRJ_EUNSUPPORTED = -4
-ABI_VERSION = 6
+ABI_VERSION = 7
 SLAB_FLAG_WORDS = 8
 
 BC_KINDS = {"fixed": 0, "mirror": 1, "periodic": 2, "face_dirichlet": 3}
@@ -110,6 +110,7 @@ _SIGNATURES = {
     "srj_slab_reset": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "srj_slab_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "srj_slab_plan": (ctypes.c_void_p, [ctypes.c_void_p]),
+    "srj_slab_direct": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "srj_slab_run": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
                                     ctypes.c_int32, _c_dp, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_int64, ctypes.c_int32,

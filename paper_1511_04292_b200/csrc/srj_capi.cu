@@ -178,16 +178,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-Kernel2D pick2d(int T, bool var, bool nl, bool recip, int bcf) {
+Kernel2D pick2d(int T, bool var, bool nl, bool recip, int bcf, bool send = false) {
   switch (T) {
-    case 1: return pick2d_t<1>(var, nl, recip, bcf);
-    case 2: return pick2d_t<2>(var, nl, recip, bcf);
-    case 3: return pick2d_t<3>(var, nl, recip, bcf);
-    case 4: return pick2d_t<4>(var, nl, recip, bcf);
-    case 5: return pick2d_t<5>(var, nl, recip, bcf);
-    case 6: return pick2d_t<6>(var, nl, recip, bcf);
-    case 7: return pick2d_t<7>(var, nl, recip, bcf);
-    default: return pick2d_t<8>(var, nl, recip, bcf);
+    case 1: return pick2d_t<1>(var, nl, recip, bcf, send);
+    case 2: return pick2d_t<2>(var, nl, recip, bcf, send);
+    case 3: return pick2d_t<3>(var, nl, recip, bcf, send);
+    case 4: return pick2d_t<4>(var, nl, recip, bcf, send);
+    case 5: return pick2d_t<5>(var, nl, recip, bcf, send);
+    case 6: return pick2d_t<6>(var, nl, recip, bcf, send);
+    case 7: return pick2d_t<7>(var, nl, recip, bcf, send);
+    default: return pick2d_t<8>(var, nl, recip, bcf, send);
   }
 }
 
@@ -750,7 +750,7 @@ static int run_cluster2d(srj_plan &plan, const double *src, double *dst, const d
 static bool direct_send_ok(const srj_plan &plan, int T) {
   const srj_plan_desc &d = plan.d;
   if (d.coef_mode != 0 || plan.has_bc) return false;
-  if (d.layout.ndim == 2) return true;
+  if (d.layout.ndim == 2) return T <= kMaxFuseSend;
   return T <= 2 && !rs3d_disabled();
 }
 
@@ -850,7 +850,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
       for (int side = 0; side < 2; ++side)
         if (d.bc[1][side].kind == SRJ_BC_FACE_DIRICHLET) bcf = 1;
     }
-    const Kernel2D k2 = pick2d(t, var, nl, !var && p.kinv != 0.0, bcf);
+    const Kernel2D k2 = pick2d(t, var, nl, !var && p.kinv != 0.0, bcf, send != nullptr);
     p.nbands = int((l.n[1] + k2.own - 1) / k2.own);
     // strips x bands = waves x resident warps (default one wave)
     const int bps = bps_override() > 0 ? std::min(bps_override(), k2.blocks_per_sm())
@@ -917,7 +917,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
         for (int side = 0; side < 2; ++side)
           if (d.bc[a][side].kind == SRJ_BC_FACE_DIRICHLET) bcf = 1;
     }
-    const Kernel3DTB k3 = pick3d_tb(t, nl, p.kinv != 0.0, bcf);
+    const Kernel3DTB k3 = pick3d_tb(t, nl, p.kinv != 0.0, bcf, send != nullptr);
     if (send && !k3.persistent)
       return fail(SRJ_EINVAL, "direct halo stores need the register-streaming 3D kernel");
     p.ntj = int((l.n[1] + k3.tj - 1) / k3.tj);
@@ -978,7 +978,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
     p.kinv_lo = recip_lo(d.coef[0], p.kinv);
     const bool recip = !var && p.kinv != 0.0;
-    const Kernel3D k3 = pick3d(var, nl, recip, cls);
+    const Kernel3D k3 = pick3d(var, nl, recip, cls, send != nullptr);
     const long per_strip = long(p.njg) * p.nbands;
     const long capacity = long(sm_count()) * k3.blocks_per_sm() * kWarps3D;
     // strips: best fill of whole waves, discounting the 2 halo planes per strip
@@ -1071,7 +1071,7 @@ struct srj_slab {
 // Flag operations of one phase, enqueued with ONE cuStreamBatchMemOp call
 // (executed in array order): halves the host API calls per fused launch.
 struct FlagOps {
-  CUstreamBatchMemOpParams p[4];
+  CUstreamBatchMemOpParams p[8];
   unsigned n = 0;
   void wait(uint32_t *addr, uint32_t v) {
     CUstreamBatchMemOpParams &x = p[n++];
@@ -1452,6 +1452,12 @@ int srj_slab_destroy(srj_slab *sl) {
 
 srj_plan *srj_slab_plan(srj_slab *sl) { return sl ? sl->plan : nullptr; }
 
+int srj_slab_direct(srj_slab *sl, int32_t fuse) {
+  if (!sl) return fail(SRJ_EINVAL, "null slab");
+  const int T = std::min(plan_depth(*sl->plan, fuse), sl->halo);
+  return (slab_direct_enabled() && direct_send_ok(*sl->plan, T)) ? 1 : 0;
+}
+
 int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *weights, int64_t m,
                  int64_t first, int64_t nsteps, int32_t fuse, double *const *d_norms,
                  int32_t *final_buf, void *const *streams) {
@@ -1493,6 +1499,9 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
   for (int i = 0; i < n; ++i) direct = direct && direct_send_ok(*slabs[i]->plan, T);
   if (direct) {
     int cur = src, flip = 0;
+    // flag operations pending per slab: the writes that follow launch j travel
+    // in one batch with the waits that precede launch j+1
+    std::vector<FlagOps> pend(static_cast<size_t>(n));
     for (int64_t k = 0; k < nsteps;) {
       const int t = int(std::min<int64_t>(T, nsteps - k));
       const int dst = others[src][flip];
@@ -1503,7 +1512,7 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
         cudaStream_t st = static_cast<cudaStream_t>(streams[serial ? 0 : i]);
         const srj_plan_desc &d = sl->plan->d;
         const int64_t ioff = interior_offset(d.layout);
-        FlagOps ops;
+        FlagOps &ops = pend[size_t(i)];
         PeerSend ps;
         for (int sd = 0; sd < 2; ++sd) {
           if (!sl->has[sd]) continue;
@@ -1531,8 +1540,16 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
           ops.write(sl->peer[sd].flags + kFlagArrived + (1 - sd), sl->epoch + 1);
           ops.write(sl->peer[sd].flags + kFlagDone + (1 - sd), sl->epoch + 1);
         }
-        rc = ops.flush(st);
-        if (rc != SRJ_OK) return rc;
+        // Ranks emulated in one process (n > 1) flush at once: the next slab's
+        // waits need these writes ahead of them, on one shared stream and
+        // also on distinct streams, which may share a hardware queue (a wait
+        // at its head would block the write behind it for ever -- caught by
+        // tests/test_gpu_slab_streams.py).  A real rank (n == 1) has only its
+        // own operations on the device.
+        if (n > 1 || k + t >= nsteps) {
+          rc = ops.flush(st);
+          if (rc != SRJ_OK) return rc;
+        }
         sl->epoch += 1;
       }
       k += t;

@@ -98,6 +98,7 @@ inline int sm_count() {
 
 // ------------------------------------------------------------ 2D dispatch
 constexpr int kMaxFuseBC = 4;  // 2D fused depth with MIRROR / FACE_DIRICHLET faces
+constexpr int kMaxFuseSend = 4;  // 2D fused depth of the kernels with direct halo stores (PeerSend)
 
 // One entry per kernel instantiation: launcher + resident blocks per SM
 // (registers and shared memory both counted, from the occupancy API), so the
@@ -112,7 +113,7 @@ struct Kernel2D {
 
 // one TU per depth group instantiates these (srj_k2d_t*.cu)
 template <int T>
-Kernel2D pick2d_t(bool var, bool nl, bool recip, int bcf);
+Kernel2D pick2d_t(bool var, bool nl, bool recip, int bcf, bool send);
 
 // ------------------------------------------------------------ 3D dispatch
 struct Kernel3D {
@@ -132,8 +133,10 @@ struct Kernel3DTB {
   bool persistent; // sweep3d_rs: grid = resident CTAs, equal (tile, plane) shares
 };
 
-Kernel3D pick3d(bool var, bool nl, bool recip, bool cls);  // srj_k3d.cu
-Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf);  // srj_k3d.cu
+// send: the instantiation that stores slab edge planes into the neighbours'
+// halos (PeerSend; constant stencil; T = 2: sweep3d_rs only)
+Kernel3D pick3d(bool var, bool nl, bool recip, bool cls, bool send = false);  // srj_k3d.cu
+Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf, bool send = false);  // srj_k3d.cu
 // fused T = 2 per-cell-coefficient 2D sweep (srj_kvar.cu); sets H/nbands/nstrips
 int launch_var2d_tb(VarTB2DParams p, bool nl, cudaStream_t st);
 int launch_gs(const GSParams &p, int nd, bool var, bool recip, int nstrips, cudaStream_t st);  // srj_kgs.cu

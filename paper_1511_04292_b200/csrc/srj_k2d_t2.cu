@@ -2,5 +2,5 @@
 #include "srj_k2d_impl.cuh"
 
 namespace srj_host {
-template Kernel2D pick2d_t<2>(bool, bool, bool, int);
+template Kernel2D pick2d_t<2>(bool, bool, bool, int, bool);
 }  // namespace srj_host

@@ -2,8 +2,8 @@
 #include "srj_k2d_impl.cuh"
 
 namespace srj_host {
-template Kernel2D pick2d_t<5>(bool, bool, bool, int);
-template Kernel2D pick2d_t<6>(bool, bool, bool, int);
-template Kernel2D pick2d_t<7>(bool, bool, bool, int);
-template Kernel2D pick2d_t<8>(bool, bool, bool, int);
+template Kernel2D pick2d_t<5>(bool, bool, bool, int, bool);
+template Kernel2D pick2d_t<6>(bool, bool, bool, int, bool);
+template Kernel2D pick2d_t<7>(bool, bool, bool, int, bool);
+template Kernel2D pick2d_t<8>(bool, bool, bool, int, bool);
 }  // namespace srj_host

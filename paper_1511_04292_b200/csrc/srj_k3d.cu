@@ -5,16 +5,16 @@
 
 namespace srj_host {
 
-template <bool VAR, bool NL, bool RECIP, bool CLS = false>
+template <bool VAR, bool NL, bool RECIP, bool CLS = false, bool SEND = false>
 struct K3 {
   static void launch(const Sweep3DParams &p, int blocks, cudaStream_t s) {
-    sweep3d<VAR, NL, RECIP, CLS><<<blocks, kWarps3D * 32, 0, s>>>(p);
+    sweep3d<VAR, NL, RECIP, CLS, SEND><<<blocks, kWarps3D * 32, 0, s>>>(p);
   }
   static int bps() {
     static std::atomic<int> cache[kMaxDevices];
     return cached_per_device(cache, [] {
       int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d<VAR, NL, RECIP, CLS>, kWarps3D * 32, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d<VAR, NL, RECIP, CLS, SEND>, kWarps3D * 32, 0);
       return n > 0 ? n : 1;
     });
   }
@@ -66,27 +66,27 @@ Kernel3DTB pick3d_tb_t(bool nl, bool recip, int bcf) {
 }
 
 // register-streaming T = 2 kernel (srj_sweep3d_rs.cuh): FIXED faces
-template <bool NL, bool RECIP>
+template <bool NL, bool RECIP, bool SEND = false>
 struct K3RS {
   using B = RS3D;
   static void configure() {
     static std::atomic<uint64_t> done{0};
     once_per_device(done, [] {
-      cudaFuncSetAttribute(sweep3d_rs<NL, RECIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(sweep3d_rs<NL, RECIP, SEND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(B::smem_bytes()));
     });
   }
   static void launch(const Sweep3DTBParams &p, const CUtensorMap &tu, const CUtensorMap &tf,
                      int blocks, cudaStream_t s) {
     configure();
-    sweep3d_rs<NL, RECIP><<<blocks, B::THREADS, B::smem_bytes(), s>>>(p, tu, tf);
+    sweep3d_rs<NL, RECIP, SEND><<<blocks, B::THREADS, B::smem_bytes(), s>>>(p, tu, tf);
   }
   static int bps() {
     static std::atomic<int> cache[kMaxDevices];
     return cached_per_device(cache, [] {
       configure();
       int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d_rs<NL, RECIP>, B::THREADS,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep3d_rs<NL, RECIP, SEND>, B::THREADS,
                                                     B::smem_bytes());
       return n > 0 ? n : 1;
     });
@@ -96,7 +96,11 @@ struct K3RS {
   }
 };
 
-Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf) {
+Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf, bool send) {
+  if (send && T == 2 && bcf == 0 && !rs3d_disabled()) {
+    if (recip) return nl ? K3RS<true, true, true>::get() : K3RS<false, true, true>::get();
+    return nl ? K3RS<true, false, true>::get() : K3RS<false, false, true>::get();
+  }
   if (T == 2 && bcf == 0 && !rs3d_disabled()) {
     if (recip) return nl ? K3RS<true, true>::get() : K3RS<false, true>::get();
     return nl ? K3RS<true, false>::get() : K3RS<false, false>::get();
@@ -107,7 +111,11 @@ Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf) {
   }
 }
 
-Kernel3D pick3d(bool var, bool nl, bool recip, bool cls) {
+Kernel3D pick3d(bool var, bool nl, bool recip, bool cls, bool send) {
+  if (send && !var) {
+    if (recip) return nl ? K3<false, true, true, false, true>::get() : K3<false, false, true, false, true>::get();
+    return nl ? K3<false, true, false, false, true>::get() : K3<false, false, false, false, true>::get();
+  }
   if (var && cls) return nl ? K3<true, true, false, true>::get() : K3<true, false, false, true>::get();
   if (var) return nl ? K3<true, true, false>::get() : K3<true, false, false>::get();
   if (recip) return nl ? K3<false, true, true>::get() : K3<false, false, true>::get();

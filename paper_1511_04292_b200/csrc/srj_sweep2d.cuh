@@ -241,7 +241,10 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-template <int T, int V, bool VAR, bool NL, bool RECIP, int BCF>
+// SEND: slab ranks' copy of the kernel that also stores the edge rows into
+// the neighbours' halo rows (PeerSend); every other instantiation carries no
+// trace of it.
+template <int T, int V, bool VAR, bool NL, bool RECIP, int BCF, bool SEND = false>
 __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
     sweep2d_tb(const __grid_constant__ Sweep2DParams p, const __grid_constant__ CUtensorMap tm_u,
                const __grid_constant__ CUtensorMap tm_f) {
@@ -448,11 +451,6 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
           }
         };
         store_row(out);
-        // slab edge rows: the same cells into the neighbour's halo row
-        if (rs < p.send.lo_end)
-          store_row(p.send.lo + int64_t(rs + p.send.lo_shift) * p.pitch + lane_col);
-        if (rs >= p.send.hi_beg)
-          store_row(p.send.hi + int64_t(rs + p.send.hi_shift) * p.pitch + lane_col);
       }
       out += p.pitch;
     }
@@ -461,6 +459,32 @@ __global__ void __launch_bounds__(Band2D<T, V>::WARPS * 32)
       fence_proxy_async();
       issue(g + NU);
     }
+  }
+
+  // Slab edge rows (SEND): each lane copies the cells it stored in rows next
+  // to a neighbour rank into that neighbour's halo rows -- after the tick
+  // loop, so the loop is the plain kernel's (a send test inside it cost 6%).
+  if constexpr (SEND) {
+    auto send_rows = [&](double *peer, int shift, int rb, int re) {
+#pragma unroll 1
+      for (int r = max(rb, i0); r < min(re, i1); ++r) {
+        const double *srow = p.dst + int64_t(r) * p.pitch + lane_col;
+        double *drow = peer + int64_t(r + shift) * p.pitch + lane_col;
+        if (lane_owned) {
+#pragma unroll
+          for (int v = 0; v < V; v += 2)
+            *reinterpret_cast<double2 *>(drow + v) = *reinterpret_cast<const double2 *>(srow + v);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const int col = lane_col + v;
+            if (col >= own_c0 && col < own_c1) drow[v] = srow[v];
+          }
+        }
+      }
+    };
+    send_rows(p.send.lo, p.send.lo_shift, p.own_b, p.send.lo_end);
+    send_rows(p.send.hi, p.send.hi_shift, p.send.hi_beg, p.own_e);
   }
 
   // per-step norms: in interior bands the fast ticks accumulate every lane

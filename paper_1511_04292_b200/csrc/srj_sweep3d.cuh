@@ -42,7 +42,9 @@ constexpr int kRows3D = 2;  // J: axis-1 rows per warp
 // constant along axis 0 / axis 2 are read at i = 0 / k = 0 (L1 / L2 hits
 // instead of HBM); a separate instantiation so the all-per-cell path keeps
 // its single offset per cell.
-template <bool VAR, bool NL, bool RECIP, bool CLS = false>
+// SEND (!VAR): slab ranks' copy that also stores the edge planes into the
+// neighbours' halo planes (PeerSend).
+template <bool VAR, bool NL, bool RECIP, bool CLS = false, bool SEND = false>
 __global__ void __launch_bounds__(kWarps3D * 32)
     sweep3d(const __grid_constant__ Sweep3DParams p) {
   constexpr int V = 2, BAND = 64, J = kRows3D;  // cells per lane, cells per band
@@ -172,12 +174,13 @@ __global__ void __launch_bounds__(kWarps3D * 32)
             }
           };
           store_row(out + int64_t(q) * p.pitch);
-          // slab edge planes: the same cells into the neighbour's halo plane
-          const int64_t inplane = int64_t(j0 + q) * p.pitch + col;
-          if (i < p.send.lo_end)
-            store_row(p.send.lo + int64_t(i + p.send.lo_shift) * p.plane + inplane);
-          if (i >= p.send.hi_beg)
-            store_row(p.send.hi + int64_t(i + p.send.hi_shift) * p.plane + inplane);
+          if constexpr (SEND) {  // slab edge planes: the same cells into the neighbour's halo
+            const int64_t inplane = int64_t(j0 + q) * p.pitch + col;
+            if (i < p.send.lo_end)
+              store_row(p.send.lo + int64_t(i + p.send.lo_shift) * p.plane + inplane);
+            if (i >= p.send.hi_beg)
+              store_row(p.send.hi + int64_t(i + p.send.hi_shift) * p.plane + inplane);
+          }
         }
         um[q] = uc[q];
         uc[q] = ud[q];

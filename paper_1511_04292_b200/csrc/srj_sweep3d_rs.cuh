@@ -86,7 +86,9 @@ __device__ __forceinline__ void tma_box_2d(void *dst, const CUtensorMap *map, in
       : "memory");
 }
 
-template <bool NL, bool RECIP>
+// SEND: slab ranks' copy that also stores the edge planes into the
+// neighbours' halo planes (PeerSend).
+template <bool NL, bool RECIP, bool SEND = false>
 __global__ void __launch_bounds__(RS3D::THREADS, 2)
     sweep3d_rs(const __grid_constant__ Sweep3DTBParams p, const __grid_constant__ CUtensorMap tm_u,
                const __grid_constant__ CUtensorMap tm_f) {
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(RS3D::THREADS, 2)
     // slab edge planes (a few per launch): every thread copies the cells it
     // just stored into the neighbour's halo plane -- outside the stage code,
     // so the hot path keeps its registers and instruction count
-    if (po2 && (pl2 < p.send.lo_end || pl2 >= p.send.hi_beg)) {
+    if (SEND && po2 && (pl2 < p.send.lo_end || pl2 >= p.send.hi_beg)) {
       auto send_plane = [&](double *peer, int shift) {
         double *rrow = peer + int64_t(pl2 + shift) * p.plane + g0;
 #pragma unroll

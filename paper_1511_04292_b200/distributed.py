@@ -319,6 +319,15 @@ class DeviceSlab:
     def run_chunk(self, src, weights, first, n, fuse=0):
         return run_slabs([self], src, weights, first, n, fuse)
 
+    def direct(self, fuse=0):
+        """True when ``run_chunk`` takes the direct data path: one launch per
+        fused step whose kernel stores the edge rows into the neighbours'
+        halos (``srj_slab_direct``, include/srj.h)."""
+        rc = self.lib.srj_slab_direct(self.handle, int(fuse))
+        if rc < 0:
+            _lib.check(rc, "srj_slab_direct")
+        return rc == 1
+
     def norms(self, n):
         return self.grid.norms[:2 * n].view(n, 2).cpu().numpy()
 

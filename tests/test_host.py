@@ -106,9 +106,6 @@ def test_argument_errors_precede_device_use():
 
 
 def test_unsupported_features_raise():
-    p = G.GridProblem(**_kw((4,)))
-    with pytest.raises(NotImplementedError):
-        G.srj_solve(p, type("C", (), {"weight_sequence": np.ones(1)})(), 1e-6)
     q = G.GridProblem(**_kw((4, 4), bc=((G.MIRROR, G.MIRROR),) * 2))
 
     def computing_hook(u):
@@ -129,6 +126,9 @@ def test_no_cpu_fallback_without_cuda():
     p = G.GridProblem(**_kw((8, 8)))
     with pytest.raises(RuntimeError, match="CUDA"):
         G.jacobi_solve(p, 1e-6)
+    line = G.GridProblem(**_kw((4,)))  # 1-D grids are on the GPU path too (grids._LineGrid)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        G.srj_solve(line, type("C", (), {"weight_sequence": np.ones(1)})(), 1e-6)
 
 
 def test_post_sweep_gather_probe():
