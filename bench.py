@@ -743,8 +743,36 @@ def run_gpu(args):
         # headline metric above is the --workload's)
         line["other_workloads"] = [measure_secondary(x, *SECONDARY[x]) for x in
                                    args.secondary.split(",") if x != args.workload]
+    if ws == 1 and args.rank_proxy:
+        line["multi_gpu_rank_proxy"] = measure_rank_proxy()
     print(json.dumps(line), flush=True)
     return 0
+
+
+def measure_rank_proxy():
+    """One rank of the multi-GPU slab path, timed on this one GPU
+    (tools/slab_rank_probe.py): the middle rank of a 3-rank decomposition runs
+    the real srj_slab_run -- the sweep kernel storing its edge rows into the
+    neighbours' halo rows, the flag-word stream operations -- against two
+    virtual neighbours on the same device, compared with the same rows as one
+    whole grid.  Excludes the NVLink latency and waiting for a slower rank."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import slab_rank_probe as srp
+
+    cases = [("cfg2 weak scaling: 4096 x 4096 rows per GPU", "cfg2", (4096, 4096), 4, 2000),
+             ("cfg4 at 8 GPUs: 4096 x 32768 rows per GPU", "cfg4", (4096, 32768), 4, 200),
+             ("cfg3 at 8 GPUs: 64 planes of 512^2 per GPU", "cfg3", (64, 512, 512), 2, 800),
+             ("cfg5 at 8 GPUs: 32 planes of 256^2 per GPU", "cfg5", (32, 256, 256), 2, 1600)]
+    out = []
+    for label, wl, own, fuse, steps in cases:
+        r = srp.probe(wl, own, fuse, steps, reps=2, modes=("direct_store",))
+        out.append({"case": label, "rank_glups": r["direct_store_glups"],
+                    "whole_grid_glups": r["whole_grid_glups"],
+                    "rank_efficiency": r["direct_store_efficiency"], "fuse": fuse})
+    return {"what": "per-rank device timeline of srj_slab_run on ONE GPU against virtual "
+                    "neighbours (no NVLink latency, no waiting for other ranks); efficiency = "
+                    "time of the same rows as one whole grid / time of the rank",
+            "cases": out}
 
 
 def main():
@@ -762,6 +790,8 @@ def main():
     ap.add_argument("--no-ttr", action="store_true")
     ap.add_argument("--secondary", default="cfg3,cfg5",
                     help="N=1: also time these workloads device-resident (empty: none)")
+    ap.add_argument("--no-rank-proxy", dest="rank_proxy", action="store_false",
+                    help="N=1: skip the one-GPU timing of a multi-GPU slab rank")
     ap.add_argument("--slab", action="store_true",
                     help="use the multi-GPU slab path even on one GPU (testing)")
     ap.add_argument("--dry-run", action="store_true",

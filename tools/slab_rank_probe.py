@@ -44,6 +44,51 @@ def timed(fn, reps):
     return a.elapsed_time(b) * 1e-3 / reps
 
 
+MODES = {"direct_store": {}, "split_streams": {"SRJ_SLAB_DIRECT": "0"},
+         "one_stream": {"SRJ_SLAB_DIRECT": "0", "SRJ_SLAB_SPLIT": "0"}}
+
+
+def probe(workload, own, fuse=0, steps=1000, reps=3, modes=tuple(MODES)):
+    """Efficiency of one slab rank owning ``own`` rows x the other axes
+    (module docstring); returns a dict for one JSON line."""
+    own = tuple(int(x) for x in own)
+    nd = len(own)
+    w = config_schedule(workload).weight_sequence
+    halo = default_halo(nd, fuse)
+    cells = int(np.prod(own))
+
+    # the same rows as one whole grid (no neighbours)
+    f = config_fields(workload, own)
+    g = DeviceGrid(f["u"], f["source"], f["center"], f["lower"], f["upper"], kappa=f.get("kappa"))
+    t_whole = timed(lambda: g.run(0, w, 0, steps, fuse), reps)
+    g.close()
+
+    # middle rank of three, virtual neighbours
+    gshape = (3 * own[0],) + own[1:]
+    d = SlabDecomposition(gshape[0], 3, 1, halo)
+    out = {"workload": workload, "owned": list(own), "fuse": fuse, "halo": halo, "steps": steps,
+           "whole_grid_glups": round(cells * steps / t_whole / 1e9, 2)}
+    for key in modes:
+        env = MODES[key]
+        os.environ.update(env)
+        try:
+            slab = DeviceSlab(slab_config_fields(workload, d, gshape))
+            lo, hi = (DeviceSlab(slab_config_fields(workload, d, gshape)) for _ in range(2))
+            slab.connect_local(lo, hi)
+            slab.reset()
+            slab.grid.flags.fill_(0x7FFFFFF0)  # every flag wait is already satisfied
+            torch.cuda.synchronize()
+            t = timed(lambda: run_slabs([slab], 0, w, 0, steps, fuse), reps)
+            out[key + "_glups"] = round(cells * steps / t / 1e9, 2)
+            out[key + "_efficiency"] = round(t_whole / t, 4)
+            for s in (slab, lo, hi):
+                s.close()
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("workload")
@@ -52,41 +97,8 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
-    own = tuple(args.shape)
-    nd = len(own)
-    w = config_schedule(args.workload).weight_sequence
-    halo = default_halo(nd, args.fuse)
-    cells = int(np.prod(own))
-
-    # the same rows as one whole grid (no neighbours)
-    f = config_fields(args.workload, own)
-    g = DeviceGrid(f["u"], f["source"], f["center"], f["lower"], f["upper"], kappa=f.get("kappa"))
-    t_whole = timed(lambda: g.run(0, w, 0, args.steps, args.fuse), args.reps)
-    g.close()
-
-    # middle rank of three, virtual neighbours
-    gshape = (3 * own[0],) + own[1:]
-    d = SlabDecomposition(gshape[0], 3, 1, halo)
-    out = {"workload": args.workload, "owned": own, "fuse": args.fuse, "halo": halo,
-           "steps": args.steps, "whole_grid_glups": cells * args.steps / t_whole / 1e9}
-    modes = (("direct_store", {}), ("split_streams", {"SRJ_SLAB_DIRECT": "0"}),
-             ("one_stream", {"SRJ_SLAB_DIRECT": "0", "SRJ_SLAB_SPLIT": "0"}))
-    for key, env in modes:
-        os.environ.update(env)
-        slab = DeviceSlab(slab_config_fields(args.workload, d, gshape))
-        lo, hi = (DeviceSlab(slab_config_fields(args.workload, d, gshape)) for _ in range(2))
-        slab.connect_local(lo, hi)
-        slab.reset()
-        slab.grid.flags.fill_(0x7FFFFFF0)  # every flag wait is already satisfied
-        torch.cuda.synchronize()
-        t = timed(lambda: run_slabs([slab], 0, w, 0, args.steps, args.fuse), args.reps)
-        out[key + "_glups"] = round(cells * args.steps / t / 1e9, 2)
-        out[key + "_efficiency"] = round(t_whole / t, 4)
-        for s in (slab, lo, hi):
-            s.close()
-        for k in env:
-            os.environ.pop(k)
-    print(json.dumps(out), flush=True)
+    print(json.dumps(probe(args.workload, args.shape, args.fuse, args.steps, args.reps)),
+          flush=True)
 
 
 if __name__ == "__main__":
