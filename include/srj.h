@@ -77,6 +77,7 @@ int srj_layout(int32_t ndim, const int64_t *n, int32_t halo0,
  *     _WJ_KERNELS[ndim](u, scratch, *_coefficient_args(problem), omega, reverse)
  *     (grids.py:478, :547-554; argument order = _coefficient_args,
  *      grids.py:482-488)
+ * for ndim = 1, 2, 3 (_wj1 / _wj2 / _wj3, grids.py:331-408).
  * u/un: device, shape n+2 per axis (dense C order).  s, c, lower[ax],
  * upper[ax]: device, interior-shaped dense.  act: device uint8 interior mask or
  * NULL.  Writes only the interior of un.  d_norms (device, 2 doubles) receives

@@ -343,8 +343,8 @@ int srj_layout(int32_t ndim, const int64_t *n, int32_t halo0, srj_layout_t *out)
 int srj_wj_dense(int32_t ndim, const int64_t *n, const double *u, double *un, const double *s,
                  const double *c, const double *const *lower, const double *const *upper,
                  const uint8_t *act, double omega, double *d_norms, void *stream) {
-  if (ndim != 2 && ndim != 3)
-    return fail(SRJ_EUNSUPPORTED, "the GPU path supports 2- and 3-dimensional grids (got %d)", ndim);
+  if (ndim < 1 || ndim > 3)
+    return fail(SRJ_EUNSUPPORTED, "the dense kernel supports 1- to 3-dimensional grids (got %d)", ndim);
   if (!u || !un || !s || !c || !lower || !upper || !d_norms) return fail(SRJ_EINVAL, "null argument");
   DenseParams p{};
   p.u = u;
@@ -358,7 +358,7 @@ int srj_wj_dense(int32_t ndim, const int64_t *n, const double *u, double *un, co
   p.act = act;
   p.ndim = ndim;
   p.n0 = n[0];
-  p.n1 = n[1];
+  p.n1 = (ndim >= 2) ? n[1] : 1;
   p.n2 = (ndim == 3) ? n[2] : 1;
   p.omega = omega;
   p.norms = d_norms;

@@ -38,6 +38,15 @@ __device__ __forceinline__ double nl_source(double kappa, double psi) {
 }
 
 // 5-point residual in the reference association order (grids.py:361-367).
+// _wj1 (grids.py:331-348): r = s - ((c*u + am0*u[i-1]) + ap0*u[i+1])
+__device__ __forceinline__ double resid3(double s, double c, double uc, double am0, double um0,
+                                         double ap0, double up0) {
+  double acc = __dmul_rn(c, uc);
+  acc = __dadd_rn(acc, __dmul_rn(am0, um0));
+  acc = __dadd_rn(acc, __dmul_rn(ap0, up0));
+  return __dsub_rn(s, acc);
+}
+
 __device__ __forceinline__ double resid5(double s, double c, double uc,
                                          double am0, double um, double ap0,
                                          double up, double am1, double uw,

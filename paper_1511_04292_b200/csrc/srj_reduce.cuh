@@ -276,7 +276,7 @@ struct DenseParams {
   const double *lo[3], *hi[3];
   const uint8_t *act;
   int ndim;
-  int64_t n0, n1, n2;  // 2D: n2 == 1
+  int64_t n0, n1, n2;  // 1D: n1 == n2 == 1; 2D: n2 == 1
   double omega;
   double *norms;
 };
@@ -288,7 +288,10 @@ __global__ void __launch_bounds__(256) wj_dense(const __grid_constant__ DensePar
        q += int64_t(gridDim.x) * blockDim.x) {
     int64_t g;  // offset of the cell in the ghosted array
     int64_t s0, s1;  // ghosted strides of axis 0 / axis 1
-    if (p.ndim == 2) {
+    if (p.ndim == 1) {
+      s0 = s1 = 1;
+      g = q + 1;
+    } else if (p.ndim == 2) {
       const int64_t i = q / p.n1, j = q % p.n1;
       s1 = 1;
       s0 = p.n1 + 2;
@@ -306,7 +309,9 @@ __global__ void __launch_bounds__(256) wj_dense(const __grid_constant__ DensePar
       continue;
     }
     double r;
-    if (p.ndim == 2)
+    if (p.ndim == 1)
+      r = resid3(p.s[q], p.c[q], uc, p.lo[0][q], p.u[g - 1], p.hi[0][q], p.u[g + 1]);
+    else if (p.ndim == 2)
       r = resid5(p.s[q], p.c[q], uc, p.lo[0][q], p.u[g - s0], p.hi[0][q], p.u[g + s0],
                  p.lo[1][q], p.u[g - 1], p.hi[1][q], p.u[g + 1]);
     else
