@@ -1025,6 +1025,7 @@ struct DriverOps {
   PFN_cuMemGetAddressRange_v3020 addr_range = nullptr;
   PFN_cuStreamBatchMemOp_v11070 batch = nullptr;
   bool ok = false;
+  bool ops64 = false;  // 64-bit wait / write stream operations on the current device
 };
 
 static const DriverOps &driver_ops() {
@@ -1044,6 +1045,14 @@ static const DriverOps &driver_ops() {
       ops.addr_range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(c);
       ops.batch = reinterpret_cast<PFN_cuStreamBatchMemOp_v11070>(e);
       ops.ok = true;
+      void *g = nullptr;
+      cudaDriverEntryPointQueryResult q5;
+      int dev = 0, v = 0;
+      if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &g, cudaEnableDefault, &q5) == cudaSuccess &&
+          q5 == cudaDriverEntryPointSuccess && cudaGetDevice(&dev) == cudaSuccess &&
+          reinterpret_cast<PFN_cuDeviceGetAttribute_v2000>(g)(
+              &v, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, dev) == CUDA_SUCCESS)
+        ops.ops64 = v != 0;
     }
     cudaGetLastError();
   });
@@ -1051,7 +1060,10 @@ static const DriverOps &driver_ops() {
 }
 
 // flag words of a rank's block (written by its neighbours)
-enum { kFlagArrived = 0, kFlagDone = 2 };  // + side (0 = from the lower, 1 = from the upper neighbour)
+// Flag words of a rank: per side (0 = written by the lower, 1 = by the upper
+// neighbour) an adjacent pair {arrived, done} -- one aligned 64-bit word, so
+// the direct path waits for / writes both with one stream operation.
+enum { kFlagArrived = 0, kFlagDone = 1 };  // + 2 * side
 
 struct srj_slab {
   srj_plan *plan = nullptr;   // the rank's plan (owned rows = desc own range)
@@ -1089,8 +1101,43 @@ struct FlagOps {
     x.writeValue.value = v;
     x.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
   }
+  // both flags of a side at once: {arrived, done} as one 64-bit word, done in
+  // the high half.  "arrived >= v and done >= v" is the unsigned 64-bit test
+  // word >= (v, v): a neighbour's done flag never runs more than one launch
+  // ahead of its arrived flag (its launch j+1 starts after its rows of launch
+  // j were delivered), so done > v implies arrived >= v.
+  void wait_pair(uint32_t *pair, uint32_t v) {
+    if (!driver_ops().ops64) {
+      wait(pair + kFlagArrived, v);
+      wait(pair + kFlagDone, v);
+      return;
+    }
+    CUstreamBatchMemOpParams &x = p[n++];
+    std::memset(&x, 0, sizeof(x));
+    x.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+    x.waitValue.address = CUdeviceptr(pair);
+    x.waitValue.value64 = (uint64_t(v) << 32) | v;
+    x.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+  }
+  void write_pair(uint32_t *pair, uint32_t v) {
+    if (!driver_ops().ops64) {
+      write(pair + kFlagArrived, v);
+      write(pair + kFlagDone, v);
+      return;
+    }
+    CUstreamBatchMemOpParams &x = p[n++];
+    std::memset(&x, 0, sizeof(x));
+    x.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+    x.writeValue.address = CUdeviceptr(pair);
+    x.writeValue.value64 = (uint64_t(v) << 32) | v;
+    x.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+  }
   int flush(cudaStream_t st) {
     if (n == 0) return SRJ_OK;
+    if (getenv("SRJ_SLAB_NOFLAGS")) {  // timing experiments only: results are undefined
+      n = 0;
+      return SRJ_OK;
+    }
     const CUresult r = driver_ops().batch(reinterpret_cast<CUstream>(st), n, p, 0);
     n = 0;
     if (r != CUDA_SUCCESS) return fail(SRJ_ECUDA, "cuStreamBatchMemOp failed (%d)", int(r));
@@ -1516,8 +1563,7 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
         PeerSend ps;
         for (int sd = 0; sd < 2; ++sd) {
           if (!sl->has[sd]) continue;
-          ops.wait(sl->flags + kFlagArrived + sd, sl->epoch);
-          ops.wait(sl->flags + kFlagDone + sd, sl->epoch);
+          ops.wait_pair(sl->flags + 2 * sd, sl->epoch);
           const srj_slab_peer &pr = sl->peer[sd];
           if (sd == 0) {
             ps.lo = pr.bufs[dst] + ioff;
@@ -1537,8 +1583,7 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
         for (int sd = 0; sd < 2; ++sd) {
           if (!sl->has[sd]) continue;
           // the neighbour sees this rank on its opposite side
-          ops.write(sl->peer[sd].flags + kFlagArrived + (1 - sd), sl->epoch + 1);
-          ops.write(sl->peer[sd].flags + kFlagDone + (1 - sd), sl->epoch + 1);
+          ops.write_pair(sl->peer[sd].flags + 2 * (1 - sd), sl->epoch + 1);
         }
         // Ranks emulated in one process (n > 1) flush at once: the next slab's
         // waits need these writes ahead of them, on one shared stream and
@@ -1593,7 +1638,7 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
       cudaStream_t es = split(sl) ? sl->edge : st;
       FlagOps ops;
       for (int sd = 0; sd < 2; ++sd)
-        if (sl->has[sd]) ops.wait(sl->flags + kFlagArrived + sd, sl->epoch);
+        if (sl->has[sd]) ops.wait(sl->flags + kFlagArrived + 2 * sd, sl->epoch);
       int rc = ops.flush(es);
       if (rc != SRJ_OK) return rc;
       if (split(sl) && k > 0) {
@@ -1621,7 +1666,7 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
       const srj_layout_t &l = sl->plan->d.layout;
       FlagOps ops;
       for (int sd = 0; sd < 2; ++sd)
-        if (sl->has[sd]) ops.wait(sl->flags + kFlagDone + sd, sl->epoch);
+        if (sl->has[sd]) ops.wait(sl->flags + kFlagDone + 2 * sd, sl->epoch);
       int rc = ops.flush(cs);
       if (rc != SRJ_OK) return rc;
       for (int sd = 0; sd < 2; ++sd) {
@@ -1632,7 +1677,7 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
                                  sl->bufs[dst] + layer_offset(l, row),
                                  sizeof(double) * size_t(sl->halo * l.plane), cudaMemcpyDefault, cs));
         // the neighbour sees this rank on its opposite side
-        ops.write(pr.flags + kFlagArrived + (1 - sd), sl->epoch + 1);
+        ops.write(pr.flags + kFlagArrived + 2 * (1 - sd), sl->epoch + 1);
       }
       rc = ops.flush(cs);
       if (rc != SRJ_OK) return rc;
@@ -1659,7 +1704,7 @@ int srj_slab_run(srj_slab *const *slabs, int32_t n, int32_t src, const double *w
       }
       FlagOps ops;
       for (int sd = 0; sd < 2; ++sd)
-        if (sl->has[sd]) ops.write(sl->peer[sd].flags + kFlagDone + (1 - sd), sl->epoch + 1);
+        if (sl->has[sd]) ops.write(sl->peer[sd].flags + kFlagDone + 2 * (1 - sd), sl->epoch + 1);
       const int rc = ops.flush(st);
       if (rc != SRJ_OK) return rc;
       // one stream for both parts: the next launches overwrite rows the
