@@ -1080,6 +1080,39 @@ struct srj_slab {
   int64_t part_b[3] = {}, part_e[3] = {};  // [0] lower edge, [1] upper edge, [2] inner (empty: b == e)
 };
 
+// Flag writes as a one-thread kernel: the fallback when the driver refuses a
+// stream write operation on a peer-mapped address (and SRJ_SLAB_FLAG_KERNEL=1
+// forces it, so the path is tested on one GPU).  System-scope release order
+// after the preceding kernel's stores is the stream order itself.
+struct FlagWrites {
+  unsigned long long addr[8];
+  unsigned long long value[8];
+  int width[8];  // 4 or 8 bytes
+  int n;
+};
+
+__global__ void flag_write_kernel(const FlagWrites w) {
+  __threadfence_system();
+  for (int i = 0; i < w.n; ++i) {
+    if (w.width[i] == 8)
+      *reinterpret_cast<volatile unsigned long long *>(w.addr[i]) = w.value[i];
+    else
+      *reinterpret_cast<volatile unsigned int *>(w.addr[i]) = static_cast<unsigned int>(w.value[i]);
+  }
+  __threadfence_system();
+}
+
+static std::atomic<int> g_flag_kernel{-1};  // -1: not decided, 0: stream operations, 1: kernel
+static bool flag_kernel_mode() {
+  int v = g_flag_kernel.load();
+  if (v < 0) {
+    const char *e = getenv("SRJ_SLAB_FLAG_KERNEL");
+    v = (e && atoi(e) == 1) ? 1 : 0;
+    g_flag_kernel.store(v);
+  }
+  return v == 1;
+}
+
 // Flag operations of one phase, enqueued with ONE cuStreamBatchMemOp call
 // (executed in array order): halves the host API calls per fused launch.
 struct FlagOps {
@@ -1138,9 +1171,61 @@ struct FlagOps {
       n = 0;
       return SRJ_OK;
     }
-    const CUresult r = driver_ops().batch(reinterpret_cast<CUstream>(st), n, p, 0);
+    if (!flag_kernel_mode()) {
+      const CUresult r = driver_ops().batch(reinterpret_cast<CUstream>(st), n, p, 0);
+      if (r == CUDA_SUCCESS) {
+        n = 0;
+        return SRJ_OK;
+      }
+      bool has_write = false;
+      for (unsigned i = 0; i < n; ++i)
+        has_write |= p[i].operation != CU_STREAM_MEM_OP_WAIT_VALUE_32 &&
+                     p[i].operation != CU_STREAM_MEM_OP_WAIT_VALUE_64;
+      if (!has_write) {
+        n = 0;
+        return fail(SRJ_ECUDA, "cuStreamBatchMemOp failed (%d)", int(r));
+      }
+      // a refused write (peer-mapped flag word): from now on write by kernel
+      cudaGetLastError();
+      g_flag_kernel.store(1);
+    }
+    // array order is kept: runs of waits go through the batch call, runs of
+    // writes through the one-thread kernel
+    unsigned i = 0;
+    while (i < n) {
+      const bool is_wait = p[i].operation == CU_STREAM_MEM_OP_WAIT_VALUE_32 ||
+                           p[i].operation == CU_STREAM_MEM_OP_WAIT_VALUE_64;
+      unsigned j = i;
+      if (is_wait) {
+        while (j < n && (p[j].operation == CU_STREAM_MEM_OP_WAIT_VALUE_32 ||
+                         p[j].operation == CU_STREAM_MEM_OP_WAIT_VALUE_64))
+          ++j;
+        const CUresult r = driver_ops().batch(reinterpret_cast<CUstream>(st), j - i, p + i, 0);
+        if (r != CUDA_SUCCESS) {
+          n = 0;
+          return fail(SRJ_ECUDA, "cuStreamBatchMemOp (waits) failed (%d)", int(r));
+        }
+      } else {
+        FlagWrites w{};
+        while (j < n && (p[j].operation == CU_STREAM_MEM_OP_WRITE_VALUE_32 ||
+                         p[j].operation == CU_STREAM_MEM_OP_WRITE_VALUE_64)) {
+          const bool wide = p[j].operation == CU_STREAM_MEM_OP_WRITE_VALUE_64;
+          w.addr[w.n] = static_cast<unsigned long long>(p[j].writeValue.address);
+          w.value[w.n] = wide ? p[j].writeValue.value64 : p[j].writeValue.value;
+          w.width[w.n] = wide ? 8 : 4;
+          ++w.n;
+          ++j;
+        }
+        flag_write_kernel<<<1, 1, 0, st>>>(w);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+          n = 0;
+          return cuda_fail(e, "flag_write_kernel");
+        }
+      }
+      i = j;
+    }
     n = 0;
-    if (r != CUDA_SUCCESS) return fail(SRJ_ECUDA, "cuStreamBatchMemOp failed (%d)", int(r));
     return SRJ_OK;
   }
 };

@@ -20,9 +20,14 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def test_flag_protocol_orders_concurrent_ranks():
+@pytest.mark.parametrize("env", [
+    {},                              # direct halo stores, flag writes as stream operations
+    {"SRJ_SLAB_FLAG_KERNEL": "1"},   # flag writes by the one-thread fallback kernel
+    {"SRJ_SLAB_DIRECT": "0"},        # staged exchange: edge / comm / inner streams per rank
+], ids=["direct", "direct-flag-kernel", "staged"])
+def test_flag_protocol_orders_concurrent_ranks(env):
     res = subprocess.run([sys.executable, os.path.join(HERE, "slab_streams_worker.py")],
-                         capture_output=True, text=True, timeout=300)
+                         capture_output=True, text=True, timeout=300, env={**os.environ, **env})
     sys.stdout.write(res.stdout)
     sys.stderr.write(res.stderr[-2000:])
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
