@@ -123,7 +123,7 @@ def test_host_entry_points_reject_null_and_bad_arguments():
     lib = _lib.load()
     n = (ctypes.c_int64 * 3)(8, 8, 0)
     ptrs = (ctypes.c_void_p * 3)()
-    assert lib.srj_wj_dense(1, n, None, None, None, None, ptrs, ptrs, None, 1.0, None,
+    assert lib.srj_wj_dense(4, n, None, None, None, None, ptrs, ptrs, None, 1.0, None,
                             None) == _lib.SRJ_EUNSUPPORTED
     assert lib.srj_wj_dense(2, n, None, None, None, None, ptrs, ptrs, None, 1.0, None,
                             None) == _lib.SRJ_EINVAL
