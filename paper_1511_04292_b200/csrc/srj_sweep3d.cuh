@@ -78,25 +78,37 @@ __global__ void __launch_bounds__(kWarps3D * 32)
       fc[q] = ld2(F(i0, q));
     }
     double *out = p.dst + int64_t(i0) * p.plane + int64_t(j0) * p.pitch + col;
+    // the centre plane's rows j0-1 / j0+J and the band-edge cells of lanes
+    // 0 / 31 are loaded one tick ahead too (they were same-tick loads whose
+    // latency every tick exposed)
+    const int eoff = lane == 0 ? -1 : 2;
+    const bool elane = lane == 0 || lane == 31;
+    double2 nrow = ld2(U(i0, -1)), srow = ld2(U(i0, J));
+    double edge[J];
+#pragma unroll
+    for (int q = 0; q < J; ++q) edge[q] = elane ? __ldg(U(i0, q) + eoff) : 0.0;
 #pragma unroll 1
     for (int i = i0; i < i1; ++i) {
       // prefetch tick i+1
       double2 udn[J], fcn[J];
+      double edgen[J];
       const int inext = min(i + 2, p.ld_hi);
+      const int icn = min(i + 1, p.ld_hi);
 #pragma unroll
       for (int q = 0; q < J; ++q) {
         udn[q] = ld2(U(inext, q));
         fcn[q] = ld2(F(i + 1, q));
+        edgen[q] = elane ? __ldg(U(icn, q) + eoff) : 0.0;
       }
-      const double2 nrow = ld2(U(i, -1));  // row j0-1 of plane i
-      const double2 srow = ld2(U(i, J));   // row j0+J of plane i
+      const double2 nrown = ld2(U(icn, -1));  // row j0-1 of plane i+1
+      const double2 srown = ld2(U(icn, J));   // row j0+J of plane i+1
       double west[J], east[J];
 #pragma unroll
       for (int q = 0; q < J; ++q) {
         west[q] = __shfl_up_sync(kFull, uc[q].y, 1);
         east[q] = __shfl_down_sync(kFull, uc[q].x, 1);
-        if (lane == 0) west[q] = U(i, q)[-1];
-        if (lane == 31) east[q] = U(i, q)[2];
+        if (lane == 0) west[q] = edge[q];
+        if (lane == 31) east[q] = edge[q];
       }
       const bool row_act = (i >= p.lo_c) && (i < p.hi_c);
       double num[J][V], y[J][V];
@@ -186,7 +198,10 @@ __global__ void __launch_bounds__(kWarps3D * 32)
         uc[q] = ud[q];
         ud[q] = udn[q];
         fc[q] = fcn[q];
+        edge[q] = edgen[q];
       }
+      nrow = nrown;
+      srow = srown;
       out += p.plane;
     }
   }
