@@ -64,6 +64,12 @@ __global__ void __launch_bounds__(kWarps2DVar * 32)
             a1 = ld2(p.am1 + o), b1 = ld2(p.ap1 + o);
     unsigned mk = mask2(o);
     double *out = p.dst + o;
+    // the band-edge neighbours of lanes 0 / 31 (columns col-1 / col+2 of the
+    // centre row) come one tick ahead as well: as same-tick loads their
+    // latency stalled the whole warp every row
+    const bool elane = lane == 0 || lane == 31;
+    const int eoff = lane == 0 ? -1 : 2;
+    double edge = elane ? __ldg(u + int64_t(i0) * pitch + eoff) : 0.0;
 #pragma unroll 1
     for (int i = i0; i < i1; ++i) {
       // prefetch tick i+1 (clamped to rows that exist; unused past i1)
@@ -73,11 +79,11 @@ __global__ void __launch_bounds__(kWarps2DVar * 32)
       const double2 fn = ld2(p.f + on), cn = ld2(p.c + on), a0n = ld2(p.am0 + on),
                     b0n = ld2(p.ap0 + on), a1n = ld2(p.am1 + on), b1n = ld2(p.ap1 + on);
       const unsigned mkn = mask2(on);
+      const double edgen = elane ? __ldg(u + int64_t(min(i + 1, p.ld_hi)) * pitch + eoff) : 0.0;
       double west = __shfl_up_sync(kFull, uc.y, 1);
       double east = __shfl_down_sync(kFull, uc.x, 1);
-      const double *row = u + int64_t(i) * pitch;
-      if (lane == 0) west = row[-1];
-      if (lane == 31) east = row[2];
+      if (lane == 0) west = edge;
+      if (lane == 31) east = edge;
       const double ucv[2] = {uc.x, uc.y}, umv[2] = {um.x, um.y}, udv[2] = {ud.x, ud.y},
                    fv[2] = {f.x, f.y}, cv[2] = {c.x, c.y}, a0v[2] = {a0.x, a0.y},
                    b0v[2] = {b0.x, b0.y}, a1v[2] = {a1.x, a1.y}, b1v[2] = {b1.x, b1.y},
@@ -112,6 +118,7 @@ __global__ void __launch_bounds__(kWarps2DVar * 32)
       a1 = a1n;
       b1 = b1n;
       mk = mkn;
+      edge = edgen;
     }
   }
   const double rm = warp_max(fabs(rmx));
