@@ -281,10 +281,101 @@ static int plan_tmap(srj_plan &plan, CUtensorMap *out, const double *base, int b
   return SRJ_OK;
 }
 
+// ---------------------------------------------------------------- scratch
+// Small device / pinned-host work buffers of a plan (norm partials, per-chunk
+// weights, gather indices, GS progress counters) come from a process-wide
+// cache instead of cudaMalloc / cudaFree per plan: a solve on a small grid
+// spent ~10 ms of its ~13 ms in those calls (each cudaFree also synchronises
+// the device).  Blocks are recycled by (device, power-of-two size); blocks
+// above kScratchMax bytes bypass the cache.  srj_plan_destroy synchronises the
+// device once before returning blocks, as cudaFree did implicitly.
+constexpr size_t kScratchMax = size_t(4) << 20;
+
+struct ScratchCache {
+  struct Block {
+    void *ptr;
+    size_t bytes;
+    int device;  // -1: pinned host
+  };
+  std::mutex mu;
+  std::vector<Block> free_list, live;
+};
+
+static ScratchCache &scratch_cache() {
+  static ScratchCache *c = new ScratchCache;  // never destroyed: no CUDA calls at exit
+  return *c;
+}
+
+static size_t scratch_round(size_t bytes) {
+  size_t r = 256;
+  while (r < bytes) r <<= 1;
+  return r;
+}
+
+static cudaError_t scratch_alloc_impl(void **out, size_t bytes, bool host) {
+  *out = nullptr;
+  const size_t want = bytes > kScratchMax ? bytes : scratch_round(bytes);
+  const int dev = host ? -1 : current_device();
+  ScratchCache &c = scratch_cache();
+  if (bytes <= kScratchMax) {
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (size_t i = 0; i < c.free_list.size(); ++i)
+      if (c.free_list[i].device == dev && c.free_list[i].bytes == want) {
+        *out = c.free_list[i].ptr;
+        c.live.push_back(c.free_list[i]);
+        c.free_list.erase(c.free_list.begin() + long(i));
+        return cudaSuccess;
+      }
+  }
+  void *ptr = nullptr;
+  const cudaError_t e = host ? cudaMallocHost(&ptr, want) : cudaMalloc(&ptr, want);
+  if (e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.live.push_back({ptr, want, dev});
+  }
+  *out = ptr;
+  return cudaSuccess;
+}
+
+template <class T>
+static cudaError_t scratch_alloc(T **out, size_t bytes) {
+  return scratch_alloc_impl(reinterpret_cast<void **>(out), bytes, false);
+}
+template <class T>
+static cudaError_t scratch_alloc_host(T **out, size_t bytes) {
+  return scratch_alloc_impl(reinterpret_cast<void **>(out), bytes, true);
+}
+
+// The caller guarantees no work in flight still uses the block.
+static void scratch_free(void *ptr) {
+  if (!ptr) return;
+  ScratchCache &c = scratch_cache();
+  ScratchCache::Block b{nullptr, 0, 0};
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (size_t i = 0; i < c.live.size(); ++i)
+      if (c.live[i].ptr == ptr) {
+        b = c.live[i];
+        c.live.erase(c.live.begin() + long(i));
+        break;
+      }
+    if (b.ptr && b.bytes <= kScratchMax && c.free_list.size() < 256) {
+      c.free_list.push_back(b);
+      return;
+    }
+  }
+  if (!b.ptr) return;  // not ours
+  if (b.device < 0)
+    cudaFreeHost(ptr);
+  else
+    cudaFree(ptr);
+}
+
 static void free_gather(srj_plan *p) {
-  if (p->g_dst) cudaFree(p->g_dst);
-  if (p->g_src) cudaFree(p->g_src);
-  if (p->g_tmp) cudaFree(p->g_tmp);
+  scratch_free(p->g_dst);
+  scratch_free(p->g_src);
+  scratch_free(p->g_tmp);
   p->g_dst = p->g_src = nullptr;
   p->g_tmp = nullptr;
   p->g_n = 0;
@@ -433,7 +524,7 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
   p->partials = nullptr;
   p->bc_scalars = nullptr;
   p->resid_blocks = std::min(4 * sm_count(), kResidBlocksMax);
-  cudaError_t e = cudaMalloc(&p->partials, sizeof(double) * 2 * p->resid_blocks);
+  cudaError_t e = scratch_alloc(&p->partials, sizeof(double) * 2 * p->resid_blocks);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "cudaMalloc(partials)");
@@ -441,11 +532,11 @@ int srj_plan_create(const srj_plan_desc *desc, srj_plan **out) {
   if (p->bc_fusable) {
     double v[6];
     for (int f = 0; f < 6; ++f) v[f] = desc->bc[f >> 1][f & 1].value;
-    e = cudaMalloc(&p->bc_scalars, sizeof(v));
+    e = scratch_alloc(&p->bc_scalars, sizeof(v));
     if (e == cudaSuccess) e = cudaMemcpy(p->bc_scalars, v, sizeof(v), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
-      cudaFree(p->partials);
-      if (p->bc_scalars) cudaFree(p->bc_scalars);
+      scratch_free(p->partials);
+      scratch_free(p->bc_scalars);
       delete p;
       return cuda_fail(e, "cudaMalloc(bc scalars)");
     }
@@ -473,9 +564,9 @@ int srj_plan_set_post_gather(srj_plan *p, const int64_t *dst, const int64_t *src
   for (int64_t i = 0; i < n && !overlap; ++i)
     overlap = std::binary_search(sorted_dst.begin(), sorted_dst.end(), src[i]);
   const size_t bytes = sizeof(int64_t) * size_t(n);
-  cudaError_t e = cudaMalloc(&p->g_dst, bytes);
-  if (e == cudaSuccess) e = cudaMalloc(&p->g_src, bytes);
-  if (e == cudaSuccess && overlap) e = cudaMalloc(&p->g_tmp, sizeof(double) * size_t(n));
+  cudaError_t e = scratch_alloc(&p->g_dst, bytes);
+  if (e == cudaSuccess) e = scratch_alloc(&p->g_src, bytes);
+  if (e == cudaSuccess && overlap) e = scratch_alloc(&p->g_tmp, sizeof(double) * size_t(n));
   if (e == cudaSuccess) e = cudaMemcpy(p->g_dst, dst, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(p->g_src, src, bytes, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -501,14 +592,15 @@ int srj_plan_set_coef_classes(srj_plan *p, const int32_t *cls) {
 int srj_plan_destroy(srj_plan *p) {
   if (!p) return SRJ_OK;
   free_gather(p);
-  if (p->gs_prog) cudaFree(p->gs_prog);
-  if (p->partials) cudaFree(p->partials);
-  if (p->row_parts) cudaFree(p->row_parts);
-  if (p->vtb_yh) cudaFree(p->vtb_yh);
-  if (p->vtb_yl) cudaFree(p->vtb_yl);
-  if (p->bc_scalars) cudaFree(p->bc_scalars);
-  if (p->d_omegas) cudaFree(p->d_omegas);
-  if (p->h_omegas) cudaFreeHost(p->h_omegas);
+  cudaDeviceSynchronize();  // nothing in flight uses the plan's buffers (cudaFree's implicit sync)
+  scratch_free(p->gs_prog);
+  scratch_free(p->partials);
+  scratch_free(p->row_parts);
+  scratch_free(p->vtb_yh);
+  scratch_free(p->vtb_yl);
+  scratch_free(p->bc_scalars);
+  scratch_free(p->d_omegas);
+  scratch_free(p->h_omegas);
   if (p->omega_ev) cudaEventDestroy(p->omega_ev);
   delete p;
   return SRJ_OK;
@@ -670,12 +762,13 @@ static int run_cluster2d(srj_plan &plan, const double *src, double *dst, const d
   const srj_plan_desc &d = plan.d;
   const srj_layout_t &l = d.layout;
   if (nsteps > plan.omega_cap) {
-    if (plan.d_omegas) cudaFree(plan.d_omegas);
-    if (plan.h_omegas) cudaFreeHost(plan.h_omegas);
+    if (plan.d_omegas || plan.h_omegas) cudaDeviceSynchronize();  // the old staging buffers
+    scratch_free(plan.d_omegas);
+    scratch_free(plan.h_omegas);
     plan.d_omegas = plan.h_omegas = nullptr;
     plan.omega_cap = 0;
-    SRJ_CUDA(cudaMalloc(&plan.d_omegas, sizeof(double) * size_t(nsteps)));
-    SRJ_CUDA(cudaMallocHost(&plan.h_omegas, sizeof(double) * size_t(nsteps)));
+    SRJ_CUDA(scratch_alloc(&plan.d_omegas, sizeof(double) * size_t(nsteps)));
+    SRJ_CUDA(scratch_alloc_host(&plan.h_omegas, sizeof(double) * size_t(nsteps)));
     if (!plan.omega_ev) SRJ_CUDA(cudaEventCreateWithFlags(&plan.omega_ev, cudaEventDisableTiming));
     plan.omega_cap = nsteps;
   } else if (plan.omega_ev) {
@@ -785,8 +878,8 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     p.ap1 = d.coef_arrays[4] + ioff;
     if (!plan.vtb_yh) {  // first fused per-cell launch: reciprocals of the centre
       const size_t bytes = sizeof(double) * size_t(l.elems);
-      SRJ_CUDA(cudaMalloc(&plan.vtb_yh, bytes));
-      SRJ_CUDA(cudaMalloc(&plan.vtb_yl, bytes));
+      SRJ_CUDA(scratch_alloc(&plan.vtb_yh, bytes));
+      SRJ_CUDA(scratch_alloc(&plan.vtb_yl, bytes));
       SRJ_CUDA(cudaMemsetAsync(plan.vtb_yh, 0, bytes, st));
       SRJ_CUDA(cudaMemsetAsync(plan.vtb_yl, 0, bytes, st));
       vtb_recip<<<sm_count() * 8, 256, 0, st>>>(d.coef_arrays[0] + ioff, plan.vtb_yh + ioff,
@@ -1346,10 +1439,13 @@ int srj_plan_residual_layers(srj_plan *plan, const double *u, double *d_layers, 
   if (l.ndim == 3) {
     const int64_t need = 2 * layers * l.n[1];
     if (need > plan->row_parts_cap) {
-      if (plan->row_parts) cudaFree(plan->row_parts);  // implicit device sync (first use)
+      if (plan->row_parts) {
+        cudaDeviceSynchronize();
+        scratch_free(plan->row_parts);
+      }
       plan->row_parts = nullptr;
       plan->row_parts_cap = 0;
-      SRJ_CUDA(cudaMalloc(&plan->row_parts, sizeof(double) * size_t(need)));
+      SRJ_CUDA(scratch_alloc(&plan->row_parts, sizeof(double) * size_t(need)));
       plan->row_parts_cap = need;
     }
     rows_out = plan->row_parts;
@@ -1403,10 +1499,13 @@ int srj_plan_gs(srj_plan *plan, double *u, double omega, int64_t nsweeps, double
   p.nstrips = nstrips;
   p.omega = omega;
   if (nstrips > plan->gs_prog_cap) {
-    if (plan->gs_prog) cudaFree(plan->gs_prog);  // implicit device sync
+    if (plan->gs_prog) {
+      cudaDeviceSynchronize();
+      scratch_free(plan->gs_prog);
+    }
     plan->gs_prog = nullptr;
     plan->gs_prog_cap = 0;
-    SRJ_CUDA(cudaMalloc(&plan->gs_prog, sizeof(unsigned long long) * size_t(nstrips)));
+    SRJ_CUDA(scratch_alloc(&plan->gs_prog, sizeof(unsigned long long) * size_t(nstrips)));
     plan->gs_prog_cap = nstrips;
   }
   p.prog = plan->gs_prog;
