@@ -87,21 +87,35 @@ __global__ void __launch_bounds__(kWarps3D * 32)
     double edge[J];
 #pragma unroll
     for (int q = 0; q < J; ++q) edge[q] = elane ? __ldg(U(i0, q) + eoff) : 0.0;
+    // running pointers of the prefetched planes (row j0): u of plane i+1 and
+    // i+2, the source of plane i+1 -- advanced by one plane per tick instead
+    // of rebuilt from 64-bit products (clamped at the ends of what exists)
+    const double *pu1 = U(min(i0 + 1, p.ld_hi), 0);
+    const double *pu2 = U(min(i0 + 2, p.ld_hi), 0);
+    const double *pf1 = F(i0 + 1, 0);
 #pragma unroll 1
     for (int i = i0; i < i1; ++i) {
       // prefetch tick i+1
       double2 udn[J], fcn[J];
       double edgen[J];
-      const int inext = min(i + 2, p.ld_hi);
-      const int icn = min(i + 1, p.ld_hi);
+      // (the per-cell instantiations keep the rebuilt addresses: with the
+      // running pointers they measured 6-15% slower)
+      const double *cu1 = VAR ? U(min(i + 1, p.ld_hi), 0) : pu1;
+      const double *cu2 = VAR ? U(min(i + 2, p.ld_hi), 0) : pu2;
+      const double *cf1 = VAR ? F(i + 1, 0) : pf1;
 #pragma unroll
       for (int q = 0; q < J; ++q) {
-        udn[q] = ld2(U(inext, q));
-        fcn[q] = ld2(F(i + 1, q));
-        edgen[q] = elane ? __ldg(U(icn, q) + eoff) : 0.0;
+        udn[q] = ld2(cu2 + q * p.pitch);
+        fcn[q] = ld2(cf1 + q * p.pitch);
+        edgen[q] = elane ? __ldg(cu1 + q * p.pitch + eoff) : 0.0;
       }
-      const double2 nrown = ld2(U(icn, -1));  // row j0-1 of plane i+1
-      const double2 srown = ld2(U(icn, J));   // row j0+J of plane i+1
+      const double2 nrown = ld2(cu1 - p.pitch);     // row j0-1 of plane i+1
+      const double2 srown = ld2(cu1 + J * p.pitch);  // row j0+J of plane i+1
+      if (!VAR) {
+        if (i + 2 <= p.ld_hi) pu1 += p.plane;
+        if (i + 3 <= p.ld_hi) pu2 += p.plane;
+        if (i + 1 >= p.lo_c && i + 2 < p.hi_c) pf1 += p.plane;
+      }
       double west[J], east[J];
 #pragma unroll
       for (int q = 0; q < J; ++q) {
