@@ -110,3 +110,22 @@ def test_line_relative_l2_rule():
     assert np.array_equal(p.u, q.u)
     assert np.allclose(hist.relative_l2[:, 1], rels, rtol=1e-12, atol=0.0)
     assert rels[-1] < 1e-8 and all(x >= 1e-8 for x in rels[:-1])
+
+
+def test_line_nonlinear_source_vs_oracle():
+    """source_kappa on a line: s(u) = kappa * u^5 re-evaluated every sweep
+    (DESIGN section 7), against the oracle's 1-D restatement."""
+    n = 777
+    rng = np.random.default_rng(5)
+    one = np.ones(n)
+    h = 1.0 / (n + 1)
+    f = {"u": np.ones(n + 2), "source": np.zeros(n), "center": 2.0 / h ** 2 * one,
+         "lower": (-one / h ** 2,), "upper": (-one / h ** 2,), "mask": None}
+    kappa = 2.0 * math.pi * rng.uniform(0.01, 0.1, n)
+    w = load_golden("const2d_p6")["weights"]
+    p, q = problem_from(f, kappa=kappa), problem_from(f)
+    hist, _ = G.srj_solve(p, Cycle(w), tol=1e-300, max_iters=120)
+    done, _, norms = oracle.run(q, w, 0, 120, kappa=kappa)
+    assert done == hist.iterations == 120
+    assert np.array_equal(p.u, q.u)
+    assert np.array_equal(hist.true_residual_inf, norms[:, 1])
