@@ -91,6 +91,22 @@ def main():
     for fuse in (1, 2):
         ok &= steps_case("3d", f3, 3, fuse, w10, 40, (0.5, 1.0))
     ok &= steps_case("3d-large", config_fields("cfg3", (96, 64, 128)), 4, 2, w10, 120, (1.0,))
+    # per-cell coefficients + masks: the staged exchange over the per-cell
+    # kernels (2D one sweep / two fused sweeps, 3D one sweep)
+    rng = np.random.default_rng(77)
+
+    def percell(shape, masked):
+        nd = len(shape)
+        return {"u": rng.standard_normal(tuple(n + 2 for n in shape)),
+                "source": rng.standard_normal(shape), "center": 2.0 * nd + rng.random(shape),
+                "lower": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd)),
+                "upper": tuple(-(0.5 + 0.5 * rng.random(shape)) for _ in range(nd)),
+                "mask": (rng.random(shape) > 0.15) if masked else None}
+
+    wv = np.concatenate([[9.0], rng.uniform(0.5, 1.0, 6)])
+    ok &= steps_case("2d-percell", percell((300, 200), True), 3, 1, wv, 41, (0.4, 1.0))
+    ok &= steps_case("2d-percell-fused", percell((260, 330), False), 4, 2, wv, 40, (0.5, 1.0))
+    ok &= steps_case("3d-percell", percell((40, 21, 70), True), 3, 1, wv, 23, (1.0,))
     for stop in ("update_inf", "residual_l2"):
         ok &= solve_case(stop, 3)
     print("ALL OK" if ok else "FAILED", flush=True)
