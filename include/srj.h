@@ -248,12 +248,13 @@ int srj_copy_layers(const srj_layout_t *lay, const double *src,
  * device through flag words in each other's memory (stream memory operations:
  * "halo of my source delivered", "neighbour finished the launch that read the
  * buffer I write into"), so the host only enqueues work.  Two data paths:
- *  - direct (default; constant stencil, 2D fused depth <= 4, 3D depth <= 2):
+ *  - direct (default; constant stencil at 2D fused depth <= 4 / 3D depth <= 2,
+ *    per-cell coefficients at depth 1):
  *    ONE launch per fused step over all owned rows; the sweep kernel itself
  *    stores the rows next to a neighbour into that neighbour's halo rows of
  *    the destination buffer (peer memory over NVLink) -- no edge launches, no
  *    copies, one batch of flag operations per launch;
- *  - staged (per-cell coefficients, deeper fusion; SRJ_SLAB_DIRECT=0): the
+ *  - staged (fused per-cell sweeps, deeper fusion; SRJ_SLAB_DIRECT=0): the
  *    edge rows run on an internal edge stream, are copied into the
  *    neighbours' halo rows (peer cudaMemcpyAsync on a comm stream) while the
  *    inner rows run concurrently on the caller's stream.
@@ -286,6 +287,11 @@ int srj_slab_reset(srj_slab *slab, void *stream);
 int srj_slab_destroy(srj_slab *slab);
 /* The slab's plan (for srj_plan_residual_layers etc.; owned by the slab). */
 srj_plan *srj_slab_plan(srj_slab *slab);
+/* Sweeps per fused launch srj_slab_run runs for this `fuse` (0 = the plan's
+ * default), capped by the halo.  A plan's default depends on its local size
+ * and coefficient mode: the ranks of a run must agree on ONE depth (their
+ * minimum) and pass it as `fuse`, or their exchanges fall out of step. */
+int srj_slab_depth(srj_slab *slab, int32_t fuse);
 /* 1 if srj_slab_run with this `fuse` takes the direct data path (one launch
  * per fused step, edge rows stored into the neighbours' halos by the sweep
  * kernel), 0 for the staged path (edge launches + peer copies), < 0 on error. */

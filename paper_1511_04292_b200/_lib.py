@@ -111,6 +111,7 @@ _SIGNATURES = {
     "srj_slab_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "srj_slab_plan": (ctypes.c_void_p, [ctypes.c_void_p]),
     "srj_slab_direct": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
+    "srj_slab_depth": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "srj_slab_run": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
                                     ctypes.c_int32, _c_dp, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_int64, ctypes.c_int32,

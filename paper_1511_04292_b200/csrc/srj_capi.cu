@@ -112,7 +112,7 @@ static void class_strides(const int32_t *cls, int a, int64_t stride, int64_t &rs
 
 static int launch_var2d(const srj_plan_desc &d, int64_t own_b, int64_t own_e, const double *cur,
                         double *nxt, const double *f, int ld_lo, int ld_hi, double omega,
-                        double *norms, cudaStream_t st) {
+                        double *norms, cudaStream_t st, const PeerSend *send = nullptr) {
   const srj_layout_t &l = d.layout;
   const int64_t ioff = interior_offset(l);
   const bool nl = d.kappa != nullptr;
@@ -156,10 +156,17 @@ static int launch_var2d(const srj_plan_desc &d, int64_t own_b, int64_t own_e, co
   p.nstrips = (rows + p.H - 1) / p.H;
   const long warps = long(p.nbands) * p.nstrips;
   const int blocks = int((warps + kWarps2DVar - 1) / kWarps2DVar);
-  if (nl)
+  if (send) {
+    p.send = *send;
+    if (nl)
+      sweep2d_var<true, true><<<blocks, kWarps2DVar * 32, 0, st>>>(p);
+    else
+      sweep2d_var<false, true><<<blocks, kWarps2DVar * 32, 0, st>>>(p);
+  } else if (nl) {
     sweep2d_var<true><<<blocks, kWarps2DVar * 32, 0, st>>>(p);
-  else
+  } else {
     sweep2d_var<false><<<blocks, kWarps2DVar * 32, 0, st>>>(p);
+  }
   SRJ_CUDA(cudaGetLastError());
   return SRJ_OK;
 }
@@ -837,12 +844,13 @@ static int run_cluster2d(srj_plan &plan, const double *src, double *dst, const d
 // launches).  Per-step (dmax, rmax) are folded into norms[2*q..] with
 // atomicMax, so several parts of one step may share a norm slot.
 // Which launches can store slab edge rows straight into the neighbours' halos
-// (PeerSend): the constant-stencil 2D band kernel at any depth, and in 3D the
-// register-streaming T = 2 kernel plus the one-sweep kernel for a chunk's odd
-// last step.
+// (PeerSend): the constant-stencil 2D band kernel up to depth kMaxFuseSend, in
+// 3D the register-streaming T = 2 kernel plus the one-sweep kernel for a
+// chunk's odd last step, and the per-cell one-sweep kernels (2D and 3D).
 static bool direct_send_ok(const srj_plan &plan, int T) {
   const srj_plan_desc &d = plan.d;
-  if (d.coef_mode != 0 || plan.has_bc) return false;
+  if (plan.has_bc) return false;
+  if (d.coef_mode != 0) return T == 1;
   if (d.layout.ndim == 2) return T <= kMaxFuseSend;
   return T <= 2 && !rs3d_disabled();
 }
@@ -854,7 +862,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
   const srj_layout_t &l = d.layout;
   const int64_t ioff = interior_offset(l);
   const bool var = d.coef_mode == 1;
-  if (send && (var || !direct_send_ok(plan, t)))
+  if (send && !direct_send_ok(plan, t))
     return fail(SRJ_EINVAL, "direct halo stores are not available for this launch");
   const bool nl = d.kappa != nullptr;
   const double *f = nl ? d.kappa : d.source;
@@ -862,7 +870,7 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
   row_ranges(d, lo_c, hi_c, ld_lo, ld_hi);
   const int rows = int(own_e - own_b);
   if (l.ndim == 2 && var && t == 1) {
-    const int rc = launch_var2d(d, own_b, own_e, cur, nxt, f, ld_lo, ld_hi, om[0], norms, st);
+    const int rc = launch_var2d(d, own_b, own_e, cur, nxt, f, ld_lo, ld_hi, om[0], norms, st, send);
     if (rc != SRJ_OK) return rc;
   } else if (l.ndim == 2 && var && t == 2 && !plan.has_bc) {
     // two fused steps on per-cell coefficients (srj_sweep2d_vtb.cuh)
@@ -1682,6 +1690,11 @@ int srj_slab_destroy(srj_slab *sl) {
 }
 
 srj_plan *srj_slab_plan(srj_slab *sl) { return sl ? sl->plan : nullptr; }
+
+int srj_slab_depth(srj_slab *sl, int32_t fuse) {
+  if (!sl) return fail(SRJ_EINVAL, "null slab");
+  return std::min(plan_depth(*sl->plan, fuse), sl->halo);
+}
 
 int srj_slab_direct(srj_slab *sl, int32_t fuse) {
   if (!sl) return fail(SRJ_EINVAL, "null slab");

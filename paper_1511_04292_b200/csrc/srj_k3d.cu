@@ -112,7 +112,9 @@ Kernel3DTB pick3d_tb(int T, bool nl, bool recip, int bcf, bool send) {
 }
 
 Kernel3D pick3d(bool var, bool nl, bool recip, bool cls, bool send) {
-  if (send && !var) {
+  if (send && var && cls) return nl ? K3<true, true, false, true, true>::get() : K3<true, false, false, true, true>::get();
+  if (send && var) return nl ? K3<true, true, false, false, true>::get() : K3<true, false, false, false, true>::get();
+  if (send) {
     if (recip) return nl ? K3<false, true, true, false, true>::get() : K3<false, false, true, false, true>::get();
     return nl ? K3<false, true, false, false, true>::get() : K3<false, false, false, false, true>::get();
   }

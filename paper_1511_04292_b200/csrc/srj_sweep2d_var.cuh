@@ -29,11 +29,14 @@ struct Var2DParams {
   int H, nbands, nstrips;
   double omega;
   double *norms;      // [2]: (dmax, rmax)
+  PeerSend send;      // slab ranks: rows also stored into the neighbours' halos
 };
 
 constexpr int kWarps2DVar = 4;
 
-template <bool NL>
+// SEND: slab ranks' copy that also stores the edge rows into the neighbours'
+// halo rows (PeerSend).
+template <bool NL, bool SEND = false>
 __global__ void __launch_bounds__(kWarps2DVar * 32)
     sweep2d_var(const __grid_constant__ Var2DParams p) {
   const int warp = threadIdx.x >> 5;
@@ -102,10 +105,17 @@ __global__ void __launch_bounds__(kWarps2DVar * 32)
           acc_absmax(dmx, d);
         }
       }
-      if (in0 && in1) {
-        *reinterpret_cast<double2 *>(out) = make_double2(y[0], y[1]);
-      } else if (in0) {
-        out[0] = y[0];
+      auto store_row = [&](double *o) {
+        if (in0 && in1) {
+          *reinterpret_cast<double2 *>(o) = make_double2(y[0], y[1]);
+        } else if (in0) {
+          o[0] = y[0];
+        }
+      };
+      store_row(out);
+      if constexpr (SEND) {  // slab edge rows: the same cells into the neighbour's halo row
+        if (i < p.send.lo_end) store_row(p.send.lo + int64_t(i + p.send.lo_shift) * pitch + col);
+        if (i >= p.send.hi_beg) store_row(p.send.hi + int64_t(i + p.send.hi_shift) * pitch + col);
       }
       out += pitch;
       um = uc;

@@ -42,7 +42,7 @@ constexpr int kRows3D = 2;  // J: axis-1 rows per warp
 // constant along axis 0 / axis 2 are read at i = 0 / k = 0 (L1 / L2 hits
 // instead of HBM); a separate instantiation so the all-per-cell path keeps
 // its single offset per cell.
-// SEND (!VAR): slab ranks' copy that also stores the edge planes into the
+// SEND: slab ranks' copy that also stores the edge planes into the
 // neighbours' halo planes (PeerSend).
 template <bool VAR, bool NL, bool RECIP, bool CLS = false, bool SEND = false>
 __global__ void __launch_bounds__(kWarps3D * 32)

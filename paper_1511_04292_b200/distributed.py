@@ -228,11 +228,33 @@ class DistComm:
         return out
 
 
+def agree_constant(slab, comm):
+    """All ranks take the constant-stencil kernels only if every rank's rows
+    allow it (a mask or varying coefficients elsewhere put every rank on the
+    per-cell kernels, so all ranks fuse the same number of sweeps per launch
+    and the exchange stays in step)."""
+    from .engine import stencil_is_constant
+
+    mine = stencil_is_constant(slab.center, slab.lower, slab.upper, slab.mask)
+    if comm.world == 1:
+        return mine
+    return bool(-comm.max_(np.array([-float(mine)]))[0] > 0.5)
+
+
+def agree_depth(backend, comm, fuse):
+    """The fused depth every rank runs: the minimum of the ranks' own depths
+    (a plan's default depends on its local size and coefficient mode)."""
+    mine = backend.depth(fuse)
+    if comm.world == 1:
+        return mine
+    return int(round(-comm.max_(np.array([-float(mine)]))[0]))
+
+
 class DeviceSlab:
     """One rank's slab on its GPU: a pooled ``DeviceGrid`` (three fields +
     flag words in one allocation) and the C slab exchange (``srj_slab_*``)."""
 
-    def __init__(self, slab, device=None):
+    def __init__(self, slab, device=None, allow_constant=True):
         from .engine import DeviceGrid
 
         d = slab.decomp
@@ -240,7 +262,7 @@ class DeviceSlab:
         self.problem = slab
         self.grid = DeviceGrid(slab.u, slab.source, slab.center, slab.lower, slab.upper,
                                active=slab.mask, kappa=slab.kappa, own=d.own_local,
-                               device=device, pooled=True)
+                               device=device, pooled=True, allow_constant=allow_constant)
         g = self.grid
         self.lib = g.lib
         self.stream = g.stream
@@ -319,6 +341,14 @@ class DeviceSlab:
     def run_chunk(self, src, weights, first, n, fuse=0):
         return run_slabs([self], src, weights, first, n, fuse)
 
+    def depth(self, fuse=0):
+        """Sweeps per fused launch this rank's plan would run for ``fuse``
+        (0 = its default), capped by the halo (``srj_slab_depth``)."""
+        rc = self.lib.srj_slab_depth(self.handle, int(fuse))
+        if rc < 1:
+            _lib.check(rc if rc < 0 else -1, "srj_slab_depth")
+        return int(rc)
+
     def direct(self, fuse=0):
         """True when ``run_chunk`` takes the direct data path: one launch per
         fused step whose kernel stores the edge rows into the neighbours'
@@ -396,18 +426,21 @@ class EmulatedRanks:
         n0 = problem.source.shape[0]
         self.decomps = [SlabDecomposition(n0, world, r, halo) for r in range(world)]
         self.concurrent = bool(concurrent)
+        from .engine import stencil_is_constant
+
+        locals_ = [SlabProblem.from_global(problem, d) for d in self.decomps]
+        const = all(stencil_is_constant(s.center, s.lower, s.upper, s.mask) for s in locals_)
         if concurrent:
             # one stream per emulated rank: launches, peer copies and flag
             # operations of different ranks race exactly as between processes
             import torch
 
             self.slabs = []
-            for d in self.decomps:
+            for sp in locals_:
                 with torch.cuda.stream(torch.cuda.Stream(device)):
-                    self.slabs.append(DeviceSlab(SlabProblem.from_global(problem, d), device))
+                    self.slabs.append(DeviceSlab(sp, device, allow_constant=const))
         else:
-            self.slabs = [DeviceSlab(SlabProblem.from_global(problem, d), device)
-                          for d in self.decomps]
+            self.slabs = [DeviceSlab(sp, device, allow_constant=const) for sp in locals_]
         for r, s in enumerate(self.slabs):
             s.connect_local(self.slabs[r - 1] if r > 0 else None,
                             self.slabs[r + 1] if r + 1 < world else None)
@@ -478,12 +511,13 @@ def _solve(problem, weights, tol, max_iters, normalise, stop, check_every, fuse,
         d = SlabDecomposition(problem.source.shape[0], comm.world, comm.rank,
                               default_halo(nd, fuse))
         slab = SlabProblem.from_global(problem, d)
-    backend = DeviceSlab(slab, device)
+    backend = DeviceSlab(slab, device, allow_constant=agree_constant(slab, comm))
     try:
         if comm.world > 1:
             backend.connect(comm)
         else:
             backend.reset()
+        fuse = agree_depth(backend, comm, fuse)
         if stop == "residual_l2" and l2_reference is None:
             if slab.kappa is not None:
                 l2_reference = lambda: l2_from_layers(  # noqa: E731 - residual of u0
@@ -540,11 +574,12 @@ class SlabGrid:
         self.comm = comm or LocalComm
         self.decomp = slab.decomp
         self.problem = slab
-        self.backend = DeviceSlab(slab, device)
+        self.backend = DeviceSlab(slab, device, allow_constant=agree_constant(slab, self.comm))
         if self.comm.world > 1:
             self.backend.connect(self.comm)
         else:
             self.backend.reset()
+        self._depths = {}
         self.stream = self.backend.stream
         self._norms = None
 
@@ -553,7 +588,9 @@ class SlabGrid:
         return self.backend.owned_cells
 
     def run(self, cur, weights, first, nsteps, fuse=0):
-        dst = self.backend.run_chunk(cur, weights, first, nsteps, fuse)
+        if fuse not in self._depths:  # one all-reduce per distinct request
+            self._depths[fuse] = agree_depth(self.backend, self.comm, fuse)
+        dst = self.backend.run_chunk(cur, weights, first, nsteps, self._depths[fuse])
         self._norms = self.comm.max_(self.backend.norms(nsteps))
         return dst
 

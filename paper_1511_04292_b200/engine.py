@@ -66,6 +66,14 @@ def coef_class(a):
     return cls
 
 
+def stencil_is_constant(center, lower, upper, active=None):
+    """True when ``DeviceGrid`` would take the constant-stencil kernels: every
+    coefficient array bitwise constant and no masked cell."""
+    if active is not None and not bool(np.all(active)):
+        return False
+    return all(constant_value(c) is not None for c in [center, *lower, *upper])
+
+
 def _contig(a, dtype):
     return np.ascontiguousarray(np.asarray(a, dtype=dtype))
 
@@ -88,7 +96,7 @@ class DeviceGrid:
 
     def __init__(self, u, source, center, lower, upper, active=None, kappa=None,
                  halo0=1, own=None, physical=(True, True), device=None, bc=None,
-                 post_gather=None, pooled=False):
+                 post_gather=None, pooled=False, allow_constant=True):
         torch = require_cuda()
         lib = _lib.load()
         self.torch = torch
@@ -132,7 +140,10 @@ class DeviceGrid:
             coefs = [center] + [x for ax in range(nd) for x in (lower[ax], upper[ax])]
             consts = [constant_value(c) for c in coefs]
             masked = active is not None and not bool(np.all(active))
-            self.constant = all(c is not None for c in consts) and not masked
+            # allow_constant=False: the ranks of a slab decomposition agreed on
+            # the per-cell kernels (another rank's rows are not constant)
+            self.constant = (all(c is not None for c in consts) and not masked
+                             and bool(allow_constant))
             if self.constant:
                 desc.coef_mode = 0
                 for i, c in enumerate(consts):

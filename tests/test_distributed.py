@@ -327,3 +327,59 @@ def test_decomposition_ranges():
     assert e[0].row_parts() == ([(11, 14)], (0, 11))
     assert e[1].row_parts() == ([(3, 6), (13, 16)], (6, 13))
     assert e[2].row_parts() == ([(3, 6)], (6, 16))
+
+
+class _DepthOnly:
+    """Stands in for DeviceSlab.depth: rank r's plan would fuse 4 - r sweeps."""
+
+    def __init__(self, rank):
+        self.rank = rank
+
+    def depth(self, fuse):
+        return fuse if fuse else 4 - self.rank
+
+
+def _agree_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1511_04292_b200.distributed import SlabProblem, agree_constant, agree_depth
+        from paper_1511_04292_b200.grids import FIXED, GridProblem
+
+        comm = DistComm()
+        n = (12, 9)
+        one = np.ones(n)
+        mask = np.ones(n, dtype=bool)
+        mask[10, 3] = False  # a masked cell in the LAST rank's rows only
+        out = {}
+        for tag, m in (("masked", mask), ("plain", None)):
+            p = GridProblem(spacing=(1.0, 1.0), u=np.zeros((14, 11)), source=one.copy(),
+                            center=4.0 * one, lower=(-one, -one), upper=(-one, -one),
+                            bc=((FIXED, FIXED),) * 2, mask=m)
+            d = SlabDecomposition(n[0], world, rank, halo=2)
+            out[tag] = agree_constant(SlabProblem.from_global(p, d), comm)
+        out["depth0"] = agree_depth(_DepthOnly(rank), comm, 0)
+        out["depth2"] = agree_depth(_DepthOnly(rank), comm, 2)
+        out_q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ranks_agree_on_kernel_family_and_depth():
+    """A mask (or varying coefficients) in one rank's rows puts EVERY rank on
+    the per-cell kernels, and every rank runs the minimum of the ranks' fused
+    depths -- otherwise the ranks would fuse different numbers of sweeps per
+    launch and their halo exchanges would fall out of step."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert results[r] == {"masked": False, "plain": True, "depth0": 3, "depth2": 2}

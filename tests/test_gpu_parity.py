@@ -361,6 +361,22 @@ def test_slab_decomposition_per_cell_coefficients(shape, world, fuse, masked):
     assert np.array_equal(norms[:, 1], hist.true_residual_inf)
 
 
+def test_slab_ranks_agree_when_only_one_slab_is_masked(table):
+    """A mask inside ONE rank's rows: every rank must take the per-cell kernels
+    (and the same fused depth), or the slabs would fuse different numbers of
+    sweeps per launch; the result is still the single-grid solve's."""
+    f = config_fields("cfg2", (120, 150))
+    mask = np.ones((120, 150), dtype=bool)
+    mask[100:110, 30:60] = False  # rows of the last of three ranks only
+    f = dict(f, mask=mask)
+    w = quantize(table.lookup(6, 4096)).weight_sequence
+    field, norms = _emulated_steps(f, 3, 0, w, 37, chunks=(0.5, 1.0))
+    p = problem_from(f)
+    hist, _ = run_steps(p, w, 37)
+    assert np.array_equal(field, p.interior)
+    assert np.array_equal(norms[:, 1], hist.true_residual_inf)
+
+
 @pytest.mark.parametrize("stop", ["update_inf", "residual_l2"])
 @pytest.mark.parametrize("world", [1, 3])
 def test_emulated_rank_solve_matches_srj_solve(table, stop, world):
