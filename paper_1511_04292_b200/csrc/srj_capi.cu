@@ -725,11 +725,21 @@ static bool cluster_schedulable_t(int C, size_t smem) {
   return ok;
 }
 
+// Shared bytes per CTA: two field slabs, plus a third with the source of the
+// owned cells when it fits (f_smem).
+constexpr size_t kClusterSmemMax = 200 * 1024;
+static size_t cluster_smem(int R, int64_t n1, bool *f_smem) {
+  const size_t slab = size_t(R + 2) * size_t(n1 + 2) * 8;
+  const bool fits = 3 * slab <= kClusterSmemMax;
+  if (f_smem) *f_smem = fits;
+  return (fits ? 3 : 2) * slab;
+}
+
 static bool cluster_schedulable(const srj_plan &plan, int C, int R) {
   const srj_plan_desc &d = plan.d;
   const bool var = d.coef_mode == 1, nl = d.kappa != nullptr;
   const bool recip = !var && recip_or_zero(d.coef[0]) != 0.0;
-  const size_t smem = 2 * size_t(R + 2) * size_t(d.layout.n[1] + 2) * 8;
+  const size_t smem = cluster_smem(R, d.layout.n[1], nullptr);
   if (var) return nl ? cluster_schedulable_t<true, true, false>(C, smem) : cluster_schedulable_t<true, false, false>(C, smem);
   if (recip) return nl ? cluster_schedulable_t<false, true, true>(C, smem) : cluster_schedulable_t<false, false, true>(C, smem);
   return nl ? cluster_schedulable_t<false, true, false>(C, smem) : cluster_schedulable_t<false, false, false>(C, smem);
@@ -819,7 +829,9 @@ static int run_cluster2d(srj_plan &plan, const double *src, double *dst, const d
   p.nsteps = int(nsteps);
   p.n1_magic = unsigned(((uint64_t(1) << 32) + uint64_t(l.n[1]) - 1) / uint64_t(l.n[1]));
   p.norms = d_norms;
-  const size_t smem = 2 * size_t(R + 2) * size_t(p.sp) * 8;
+  bool f_smem = false;
+  const size_t smem = cluster_smem(R, l.n[1], &f_smem);
+  p.f_smem = f_smem ? 1 : 0;
   p.kinv = var ? 0.0 : recip_or_zero(d.coef[0]);
   p.kinv_lo = recip_lo(d.coef[0], p.kinv);
   const bool recip = !var && p.kinv != 0.0;

@@ -58,6 +58,7 @@ struct Cluster2DParams {
   const double *bc_values[2][2];
   const double *omegas;    // [nsteps] device
   int nsteps;
+  int f_smem;              // the source (or kappa) of the owned cells sits in a third shared slab
   unsigned n1_magic;       // ceil(2^32 / n1): row of cell q = umulhi(q, n1_magic)
   double *norms;           // [nsteps][2]
 };
@@ -89,6 +90,12 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     const double v = p.src[int64_t(r0 + lr) * p.pitch + gc];
     smem_d[off(lr, gc)] = v;
     smem_d[slab + off(lr, gc)] = v;
+    // the source does not change between steps: one global read per launch
+    // instead of one (L2 latency, every step) per cell and step
+    if (p.f_smem)
+      smem_d[2 * slab + off(lr, gc)] = (lr >= 0 && lr < rows && gc >= 0 && gc < p.n1)
+                                           ? p.f[int64_t(r0 + lr) * p.pitch + gc]
+                                           : 0.0;
   }
   cluster.sync();  // every buffer loaded before the first pushes land in it
 
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       }
       double out = uc;
       if (active) {
-        const double fval = __ldg(p.f + g);
+        const double fval = p.f_smem ? smem_d[2 * slab + o] : __ldg(p.f + g);
         const double s_ = NL ? nl_source(fval, uc) : fval;
         const double rr = resid5(s_, c, uc, a0, smem_d[bc + o - sp], b0, smem_d[bc + o + sp], a1,
                                  smem_d[bc + o - 1], b1, smem_d[bc + o + 1]);
