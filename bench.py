@@ -415,7 +415,7 @@ def measure_e2e(args, ws, rank, comm, shape, sweeps, host):
     cyc = config_schedule(args.workload)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
     times = []
-    if ws == 1:
+    if isinstance(host, dict):  # one whole grid (N = 1 without --slab)
         f = host
         u = pin(f["u"])
         src = pin(f["kappa"] if "kappa" in f else f["source"])
@@ -454,7 +454,8 @@ def measure_e2e(args, ws, rank, comm, shape, sweeps, host):
             sp = D.SlabProblem(slab.decomp, slab.global_shape, u, slab.center, slab.lower,
                                slab.upper, source=None if slab.kappa is not None else src,
                                kappa=src if slab.kappa is not None else None)
-            comm.barrier()
+            if comm is not None:
+                comm.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             D.srj_solve(sp, cyc, tol=1e-300, max_iters=sweeps)

@@ -55,3 +55,22 @@ def test_bench_refuses_missing_gpus():
     assert res.returncode == 2
     line = json.loads(res.stdout.strip().splitlines()[-1])
     assert "error" in line and line["n_gpus"] == 4
+
+
+@pytest.mark.gpu
+def test_bench_slab_path_on_one_gpu():
+    """bench.py --slab: the multi-GPU code path of the bench (SlabGrid, the
+    distributed srj_solve for the end-to-end figure) with one rank."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run(
+        [sys.executable, os.path.join(root, "bench.py"), "--slab", "--workload", "cfg2", "--shape",
+         "512", "512", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-ttr", "--secondary", "",
+         "--no-rank-proxy"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["gpu_launches"] > 0
