@@ -80,6 +80,13 @@ bool slab_direct_enabled() {
   return !(e && *e && atoi(e) == 0);
 }
 
+// SRJ_MIN_PLANES=<n>: least planes per persistent CTA of the 3D T = 2 kernel (tuning knob)
+long min_planes_3d() {
+  const char *e = getenv("SRJ_MIN_PLANES");
+  const long v = e ? atol(e) : 2;
+  return v >= 1 ? v : 2;
+}
+
 // SRJ_BPS=<n>: size the 2D grid for n resident blocks per SM (tuning knob)
 int bps_override() {
   static int b = -1;
@@ -1057,8 +1064,13 @@ static int launch_fused(srj_plan &plan, int64_t own_b, int64_t own_e, const doub
     rc = plan_tmap(plan, &tf, f, k3.box_cols, k3.f_box_rows);
     if (rc != SRJ_OK) return rc;
     long blocks = tiles * p.nstrips;
-    if (k3.persistent)  // one CTA per resident slot, at least 8 planes each
-      blocks = std::max(1L, std::min(capacity, (tiles * rows + 7) / 8));
+    if (k3.persistent) {
+      // one CTA per resident slot, at least kMinPlanes planes each: a small
+      // grid is spread over more CTAs (each pays the 5-tick pipeline fill, but
+      // on SMs that would idle) -- 2 instead of 8: 64^3 12.5 -> ~7 us per sweep
+      const long min_planes = min_planes_3d();
+      blocks = std::max(1L, std::min(capacity, (tiles * rows + min_planes - 1) / min_planes));
+    }
     k3.launch(p, tu, tf, int(blocks), st);
   } else {
     Sweep3DParams p{};
