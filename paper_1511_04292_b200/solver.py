@@ -121,7 +121,9 @@ def run_solve(backend, comm, weights, tol, max_iters, normalise, stop, check_eve
         # about as much as the work so far (sized from the GLOBAL grid, so all
         # ranks take the same chunks)
         est = step_seconds_estimate(cells)
-        cap = int(min(65536, max(64, 0.05 / est)))
+        # (small grids: ~20 ms chunks -- a host check costs ~0.1 ms there, the
+        # replay of the last chunk on average half a chunk)
+        cap = int(min(65536, max(64, (0.02 if est < 2e-5 else 0.05) / est)))
         span = int(min(cap, max(32, 0.002 / est)))
     while done < max_iters:
         n = min(span, max_iters - done)
