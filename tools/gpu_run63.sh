@@ -1,0 +1,2 @@
+cd $GRAFT_REPO_ROOT
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
